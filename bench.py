@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py — FP64 KFVM-WENO cell-updates/s per RK stage on B200.
+
+Metric (BASELINE.json): FP64 cell-updates/s per RK stage; one unit of work is
+one cell x one SSP-RK3 stage.  A bench "step" is one SSP-RK3 time step (3
+stages) of the workload over the whole grid.  Default workload: BASELINE.json
+configs[1] (2-D 1024^2 outflow Voronoi, R=2, CFL 0.4); `--config k` selects
+another (1-based).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl reference]
+
+Under torchrun (N>1) each rank owns a contiguous slab of the last axis
+(halo exchange + dt allreduce through NCCL inside libkfvm_b200.so); timing is
+CUDA events on the solver stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def algorithmic_flops(rset) -> int:
+    """F = 2 nvar sum_q N_q (n_alpha + n_pts) per cell-stage."""
+    nvar = rset.dim + 2
+    return 2 * nvar * sum(st.count for st in rset.st) * (rset.n_derivs() + rset.n_face_points())
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+        return dist, rank, ws, local
+    return None, 0, 1, 0
+
+
+def cpu_sample(w, rset, seconds_target=10.0, nthreads=None):
+    """Time the CPU oracle on a bounded sub-box of the workload (planes of the
+    slab axis) and return (cell-updates/s, cores, description)."""
+    import paper_2401_16543_b200 as K
+    from oracle import Oracle  # CPU baseline leg only
+    g = w.grid
+    nthreads = nthreads or (os.cpu_count() or 1)
+    o = Oracle(g, rset, nthreads=nthreads)
+    plane = g.nx * (g.ny if g.dim == 3 else 1)
+    # planes needed around the sample: stencil + limiter halo
+    H = g.radius + 1
+    # calibrate on one plane
+    np_s = 1
+    Ub = K.initial_condition(g, w.ic, 0, min(g.slab_extent, np_s + 2 * H + 2), nthreads)
+    sub = _subgrid(g, Ub.shape[0])
+    osub = Oracle(sub, rset, nthreads=nthreads)
+    t1 = osub.sample_stage_seconds(Ub, H, np_s)
+    per_plane = max(t1, 1e-4)
+    np_s = int(max(1, min(g.slab_extent - 2 * H, seconds_target / per_plane / 3)))
+    Ub = K.initial_condition(g, w.ic, 0, np_s + 2 * H, nthreads)
+    sub = _subgrid(g, Ub.shape[0])
+    osub = Oracle(sub, rset, nthreads=nthreads)
+    times = [osub.sample_stage_seconds(Ub, H, np_s) for _ in range(3)]
+    t = min(times)
+    cells = plane * np_s
+    desc = (f"oracle stage (reconstruct+limit+Riemann+RK combine) on {np_s} of {g.slab_extent} "
+            f"slab-axis planes ({cells} cells) of the workload IC, {nthreads} threads, best of 3")
+    return cells / t, nthreads, desc, o
+
+
+def _subgrid(g, planes):
+    from dataclasses import replace
+    if g.dim == 3:
+        return replace(g, nz=planes, dx=g.dx if g.dx else 1.0 / g.nx)
+    return replace(g, ny=planes, dx=g.dx if g.dx else 1.0 / g.nx)
+
+
+def run_reference(args, w, rset, rank):
+    """--impl reference: the CPU oracle (C++ restatement of the reference
+    algorithm; the reference itself does not build) on the
+    host cores, each step a bounded sample of the workload."""
+    if rank != 0:
+        return
+    import paper_2401_16543_b200 as K
+    from oracle import Oracle
+    g = w.grid
+    nthreads = os.cpu_count() or 1
+    H = g.radius + 1
+    plane = g.nx * (g.ny if g.dim == 3 else 1)
+    # size each step to ~2 s of CPU work
+    np_s = 1
+    Ub = K.initial_condition(g, w.ic, 0, np_s + 2 * H, nthreads)
+    o = Oracle(_subgrid(g, Ub.shape[0]), rset, nthreads=nthreads)
+    t1 = o.sample_stage_seconds(Ub, H, 1)
+    np_s = int(max(1, min(g.slab_extent - 2 * H, 0.7 / max(t1, 1e-4))))
+    Ub = K.initial_condition(g, w.ic, 0, np_s + 2 * H, nthreads)
+    o = Oracle(_subgrid(g, Ub.shape[0]), rset, nthreads=nthreads)
+    for _ in range(args.warmup):
+        o.sample_stage_seconds(Ub, H, np_s)
+    tot = 0.0
+    for _ in range(args.steps):
+        tot += 3 * o.sample_stage_seconds(Ub, H, np_s)  # one step = 3 stages
+    cells = plane * np_s
+    value = cells * 3 * args.steps / tot
+    sample = (f"per step: 3 oracle stages on {np_s} of {g.slab_extent} slab-axis planes "
+              f"({cells} cells) of the workload IC")
+    line = {
+        "metric": "fp64_cell_updates_per_s_per_rk_stage", "value": value,
+        "unit": "cell-updates/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(w, args),
+        "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": nthreads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(w, args):
+    g = w.grid
+    shape = "x".join(str(x) for x in ((g.nx, g.ny, g.nz) if g.dim == 3 else (g.nx, g.ny)))
+    return {"workload": f"BASELINE config {w.index}: {g.dim}-D Euler {shape} {g.bc}, R={g.radius}, "
+                        f"{w.ic.kind} IC, SSP-RK3 CFL {g.cfl}, {g.riemann.upper()}",
+            "cells": g.ncells, "radius": g.radius, "dim": g.dim, "bc": g.bc,
+            "cfl": g.cfl, "config_steps": w.steps,
+            "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single",
+            "l2": "working set per step (3 state buffers + face-state scratch) exceeds the 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n", type=int, default=None, help="override resolution (testing)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    import paper_2401_16543_b200 as K
+    w = K.baseline_config(args.config, n=args.n)
+    if args.steps is None:
+        args.steps = w.steps
+    args.warmup = max(3, args.warmup)
+    rset = K.precompute(w.grid.radius, dim=w.grid.dim)
+    dist, rank, ws, local = dist_init()
+    args.gpus = ws if ws > 1 else args.gpus
+
+    if args.impl == "reference":
+        run_reference(args, w, rset, rank)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    nccl_id = None
+    if ws > 1:
+        from paper_2401_16543_b200.solver import nccl_unique_id
+        idt = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            idt[:] = torch.tensor(list(nccl_unique_id()), dtype=torch.uint8)
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.tolist())
+    g = w.grid
+    s = K.Solver(g, rset, rank=rank, nranks=ws, device=local, nccl_id=nccl_id)
+    stream = torch.cuda.ExternalStream(s.stream)
+
+    # warm-up (also captures the CUDA graph)
+    s.generate_ic(w.ic)
+    s.run_async(args.warmup)
+    s.sync()
+    # per-kernel timing pass (events around every launch, not graph-replayed)
+    s.set_option("timing", 1)
+    s.generate_ic(w.ic)
+    s.run_async(1)
+    s.sync()
+    kt = s.kernel_times()
+    s.set_option("timing", 0)
+    launches_per_step = None
+
+    # timed region: K steps from the workload IC
+    s.generate_ic(w.ic)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = s.launch_count
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    s.run_async(args.steps)
+    ev1.record(stream)
+    s.sync()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = s.launch_count - l0
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        dist.barrier()
+    cells = g.ncells
+    value = cells * 3 * args.steps / (ms * 1e-3)
+
+    # end-to-end through the public API with host buffers: per step upload the
+    # state from pinned host memory, one SSP-RK3 step, read the state back
+    plane = g.nx * (g.ny if g.dim == 3 else 1)
+    nloc = plane * s.np_local * g.nvar
+    host = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
+    s.generate_ic(w.ic)
+    s.get_state_device  # noqa: B018 (API presence)
+    Uh = host.numpy().reshape(s.local_shape)
+    Uh[...] = s.get_state()
+    e2e_steps = max(1, min(args.steps, 10))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        s.set_state(Uh)
+        s.ssp_rk3_step()
+        Uh[...] = s.get_state()
+    t_e2e = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([t_e2e], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t[0])
+    e2e_value = cells * 3 * e2e_steps / t_e2e
+
+    if rank == 0:
+        F = algorithmic_flops(rset)
+        peaks = measured_peaks()
+        fp64 = peaks.get("fp64_tflops")
+        fp64_src = "MEASURED_PEAKS.json fp64_tflops"
+        if fp64 is None:
+            p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+            try:
+                with open(p) as f:
+                    fp64 = json.load(f)["dfma_tflops"]
+                fp64_src = "profiles/fp64_peak.json (DFMA microbenchmark on this pool)"
+            except Exception:
+                fp64 = 37.2
+                fp64_src = "nominal 148 SM x 64 DFMA x 2 x 1.965 GHz (not measured)"
+        # dominant kernel: k_states; one launch covers one chunk of the slab
+        nstates_launch = 3 * ((s.np_local + 0) // 1)  # placeholder, replaced below
+        states_ms_per_step = kt["states"]
+        flops_per_step = F * cells * 3
+        achieved = flops_per_step / (states_ms_per_step * 1e-3) / 1e12 if states_ms_per_step else None
+        cpu = None
+        if not args.no_cpu and ws == 1:
+            v, cores, desc, _ = cpu_sample(w, rset, seconds_target=8.0)
+            cpu = {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "port",
+                   "sample": desc}
+        line = {
+            "metric": "fp64_cell_updates_per_s_per_rk_stage", "value": value,
+            "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(w, args),
+            "e2e": {"value": e2e_value, "unit": "cell-updates/s",
+                    "h2d_bytes_per_step": nloc * 8, "d2h_bytes_per_step": nloc * 8,
+                    "steps": e2e_steps, "api": "Solver.set_state/ssp_rk3_step/get_state (C-ABI)"},
+            "roofline": {"bound": "fp64", "kernel": "k_states (reconstruction+WENO-AO+limiter)",
+                         "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                         "frac": (achieved / fp64) if achieved else None,
+                         "peak_source": fp64_src,
+                         "algorithmic_flops_per_cell_stage": F,
+                         "traffic": None},
+            "kernel_ms_per_step": kt,
+            "whole_step_fp64_frac": F * value / 1e12 / fp64,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

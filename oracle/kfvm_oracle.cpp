@@ -1,0 +1,734 @@
+// kfvm_oracle.cpp — CPU oracle of the KFVM-WENO FP64 stage update.
+//
+// TEST INFRASTRUCTURE ONLY (see kfvm_oracle.h).  Compiled with
+// -ffp-contract=off: every fused multiply-add below is an explicit std::fma,
+// so the arithmetic sequence is the pinned FP contract of DESIGN.md §4 that
+// the CUDA path follows operation for operation.
+//
+// Reference anchors (S: = SPEC.md, P: = PAPER.md):
+//   pressure / sound speed / exact flux ........ S:321-349
+//   Phi, Phi^-1 (linearised primitives) ........ S:350-367
+//   smoothness indicator, weights, WENO-AO ..... S:256-282
+//   flattener, bounds, density/pressure limit .. S:410-446
+//   Roe/Batten speeds, HLL, HLLC ............... S:477-503
+//   fill_ghost (periodic/outflow) .............. S:553-561 (outflow = index clamp)
+//   reconstruct_states (KXRCF off) ............. S:562-570
+//   compute_rhs ................................ S:589-597
+//   SSP-RK3 (BASELINE.json; replaces S:598) .... Shu-Osher form
+//   select_dt .................................. S:607-615 (+|w|+c in 3-D)
+#include "kfvm_oracle.h"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+namespace {
+
+using std::fma;
+
+struct Consts {
+  int dim, nv, R, riemann, bc;
+  int n[3];
+  double gamma, gm1, inv_gm1, dx, cfl, eps, kappa, kf, onepk, onemk;
+  double scale[32];  // Delta^(2|alpha|)
+};
+
+Consts make_consts(const kfvm_config* c, const kfvm_table* t) {
+  Consts k{};
+  k.dim = c->dim;
+  k.nv = c->dim + 2;
+  k.R = c->radius;
+  k.riemann = c->riemann;
+  k.bc = c->bc;
+  k.n[0] = c->nx;
+  k.n[1] = c->ny;
+  k.n[2] = c->dim == 3 ? c->nz : 1;
+  k.gamma = c->gamma;
+  k.gm1 = c->gamma - 1.0;
+  k.inv_gm1 = 1.0 / (c->gamma - 1.0);
+  k.dx = c->dx;
+  k.cfl = c->cfl;
+  k.eps = c->eps;
+  k.kappa = c->kappa;
+  k.kf = c->flattener_kf;
+  k.onepk = 1.0 + c->kappa;
+  k.onemk = 1.0 - c->kappa;
+  if (t) {
+    for (int a = 0; a < t->n_alpha; ++a) {
+      const int ord = t->alpha[3 * a] + t->alpha[3 * a + 1] + t->alpha[3 * a + 2];
+      double s = 1.0;
+      for (int e = 0; e < 2 * ord; ++e) s *= c->dx;  // Delta^(2|alpha|)
+      k.scale[a] = s;
+    }
+  }
+  return k;
+}
+
+// ---------------------------------------------------------------- state algebra
+inline double pressure(int dim, const double* U, double gm1) {
+  double q = U[1] * U[1];
+  q = fma(U[2], U[2], q);
+  if (dim == 3) q = fma(U[3], U[3], q);
+  return gm1 * (U[dim + 1] - 0.5 * (q / U[0]));
+}
+
+inline double sound(double gamma, double p, double rho) {
+  return std::sqrt((gamma * p) / rho);
+}
+
+struct Transform {  // Phi / Phi^-1 at the central average
+  double rt, inv_r, ut[3], ke;
+};
+
+inline Transform make_transform(int dim, const double* Ur) {
+  Transform T;
+  T.rt = Ur[0];
+  T.inv_r = 1.0 / Ur[0];
+  T.ut[2] = 0.0;
+  for (int d = 0; d < dim; ++d) T.ut[d] = Ur[1 + d] / Ur[0];
+  double ke = T.ut[0] * T.ut[0];
+  ke = fma(T.ut[1], T.ut[1], ke);
+  if (dim == 3) ke = fma(T.ut[2], T.ut[2], ke);
+  T.ke = 0.5 * ke;
+  return T;
+}
+
+// W = Phi U, one component v (constant part dropped)
+inline double to_recon(int dim, const Transform& T, double gm1, const double* U, int v) {
+  if (v == 0) return U[0];
+  if (v <= dim) return fma(-T.ut[v - 1], U[0], U[v]) * T.inv_r;
+  double t = fma(T.ke, U[0], U[dim + 1]);
+  t = fma(-T.ut[0], U[1], t);
+  t = fma(-T.ut[1], U[2], t);
+  if (dim == 3) t = fma(-T.ut[2], U[3], t);
+  return gm1 * t;
+}
+
+// U = Phi^-1 W
+inline void from_recon(int dim, const Transform& T, double inv_gm1, const double* W, double* U) {
+  U[0] = W[0];
+  for (int d = 0; d < dim; ++d) U[1 + d] = fma(T.ut[d], W[0], T.rt * W[1 + d]);
+  double t = W[dim + 1] * inv_gm1;
+  t = fma(T.ut[0], W[1], t);
+  t = fma(T.ut[1], W[2], t);
+  if (dim == 3) t = fma(T.ut[2], W[3], t);
+  U[dim + 1] = fma(T.ke, W[0], t);
+}
+
+// ------------------------------------------------------------------- WENO-AO
+// beta_q, omega_q and the WENO-AO values at every face point for one scalar
+// field g on S0.  Dot products accumulate in stencil order.
+void weno_field(const kfvm_table* t, const Consts& k, const double* g, double* beta_out,
+                double* omega_out, double* vals) {
+  const int NS = t->n_stencils;
+  double wt[KFVM_MAX_STENCILS], c[KFVM_MAX_STENCILS];
+  for (int q = 0; q < NS; ++q) {
+    const int N = t->size[q];
+    const int* gat = t->gather + t->cell_offset[q];
+    const double* D = t->deriv + (size_t)t->cell_offset[q] * t->n_alpha;
+    double beta = 0.0;
+    for (int a = 0; a < t->n_alpha; ++a) {
+      double d = 0.0;
+      for (int h = 0; h < N; ++h) d = fma(D[a * N + h], g[gat[h]], d);
+      beta = fma(k.scale[a], d * d, beta);
+    }
+    if (beta_out) beta_out[q] = beta;
+    wt[q] = t->gamma_lin[q] / fma(beta, beta, k.eps);  // P eq. nlinWts
+  }
+  double sum = wt[0];
+  for (int q = 1; q < NS; ++q) sum = sum + wt[q];
+  double om[KFVM_MAX_STENCILS] = {0};
+  for (int q = 0; q < NS; ++q) om[q] = wt[q] / sum;
+  if (omega_out)
+    for (int q = 0; q < NS; ++q) omega_out[q] = om[q];
+  c[0] = om[0] / t->gamma_lin[0];
+  for (int q = 1; q < NS; ++q) c[q] = fma(-c[0], t->gamma_lin[q], om[q]);
+  for (int s = 0; s < t->n_points; ++s) {
+    double v = 0.0;
+    for (int q = 0; q < NS; ++q) {
+      const int N = t->size[q];
+      const int* gat = t->gather + t->cell_offset[q];
+      const double* r = t->face + (size_t)t->cell_offset[q] * t->n_points + (size_t)s * N;
+      double p = 0.0;
+      for (int h = 0; h < N; ++h) p = fma(r[h], g[gat[h]], p);
+      v = (q == 0) ? c[0] * p : fma(c[q], p, v);
+    }
+    vals[s] = v;
+  }
+}
+
+// ------------------------------------------------------- positivity limiter
+// nbr: 3^dim averages (i fastest), centre at index (3^dim)/2.  Returns 0 ok,
+// 2 if the cell average itself is inadmissible.
+int limit_cell(const Consts& k, int npts, double* st, const double* nbr, double* info) {
+  const int dim = k.dim, nv = k.nv;
+  const int nn = dim == 3 ? 27 : 9;
+  const double* Uc = nbr + (size_t)(nn / 2) * nv;
+  double rbmax = Uc[0], rbmin = Uc[0];
+  double pbmin = pressure(dim, Uc, k.gm1);
+  double cmin = sound(k.gamma, pbmin, Uc[0]);
+  for (int m = 0; m < nn; ++m) {
+    const double* U = nbr + (size_t)m * nv;
+    const double p = pressure(dim, U, k.gm1);
+    rbmax = std::fmax(rbmax, U[0]);
+    rbmin = std::fmin(rbmin, U[0]);
+    pbmin = std::fmin(pbmin, p);
+    cmin = std::fmin(cmin, sound(k.gamma, p, U[0]));
+  }
+  // undivided velocity divergence
+  auto vel = [&](int m, int d) { return nbr[(size_t)m * nv + 1 + d] / nbr[(size_t)m * nv]; };
+  const int c0 = nn / 2;
+  double delta = 0.5 * (vel(c0 + 1, 0) - vel(c0 - 1, 0));
+  delta = fma(0.5, vel(c0 + 3, 1) - vel(c0 - 3, 1), delta);
+  if (dim == 3) delta = fma(0.5, vel(c0 + 9, 2) - vel(c0 - 9, 2), delta);
+  const double kc = k.kf * cmin;
+  double eta = -(delta + kc) / kc;
+  eta = std::fmin(1.0, std::fmax(0.0, eta));
+  // bounds
+  // (1 + kappa - kappa eta) written as 1 + kappa (1 - eta) so the factor is
+  // exactly 1 at eta = 1 and the bounds always bracket the cell average
+  const double fup = fma(k.kappa, 1.0 - eta, 1.0);
+  const double flo = fma(-k.kappa, 1.0 - eta, 1.0);
+  const double rmax = rbmax * fup;
+  const double rmin = rbmin * flo;
+  const double pmin = pbmin * flo;
+  const double rt = Uc[0];
+  const double pt = pressure(dim, Uc, k.gm1);
+  if (!(rt > 0.0) || !(pt > 0.0) || !(rmin > 0.0) || !(pmin > 0.0)) return 2;
+  // density (P eq. ppThetaRho)
+  double th = 1.0;
+  for (int s = 0; s < npts; ++s) {
+    const double r = st[s * nv];
+    if (r < rmin)
+      th = std::fmin(th, (rt - rmin) / (rt - r));
+    else if (r > rmax)
+      th = std::fmin(th, (rmax - rt) / (r - rt));
+  }
+  if (th < 1.0)
+    for (int s = 0; s < npts; ++s)
+      for (int v = 0; v < nv; ++v) st[s * nv + v] = fma(th, st[s * nv + v] - Uc[v], Uc[v]);
+  // pressure by bisection (P eqs. thetapRoot/thetaP)
+  double thp = 1.0;
+  for (int s = 0; s < npts; ++s) {
+    if (pressure(dim, st + s * nv, k.gm1) < pmin) {
+      double lo = 0.0, hi = 1.0, x[5];
+      for (int it = 0; it < 100 && (hi - lo) > 1e-12 * hi; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        for (int v = 0; v < nv; ++v) x[v] = fma(mid, st[s * nv + v] - Uc[v], Uc[v]);
+        if (pressure(dim, x, k.gm1) >= pmin)
+          lo = mid;
+        else
+          hi = mid;
+      }
+      thp = std::fmin(thp, lo);
+    }
+  }
+  if (thp < 1.0)
+    for (int s = 0; s < npts; ++s)
+      for (int v = 0; v < nv; ++v) st[s * nv + v] = fma(thp, st[s * nv + v] - Uc[v], Uc[v]);
+  if (info) {
+    info[0] = eta;
+    info[1] = rmin;
+    info[2] = rmax;
+    info[3] = pmin;
+    info[4] = th;
+    info[5] = thp;
+  }
+  return 0;
+}
+
+// ----------------------------------------------------------------- Riemann
+inline void exact_flux(int dim, int d, const double* U, double un, double p, double* F) {
+  const int nv = dim + 2;
+  F[0] = U[1 + d];
+  for (int m = 0; m < dim; ++m) F[1 + m] = U[1 + m] * un;
+  F[1 + d] = F[1 + d] + p;
+  F[nv - 1] = (U[nv - 1] + p) * un;
+}
+
+struct Speeds {
+  double sl, sr;
+};
+
+inline Speeds batten(int dim, double gamma, double gm1, int d, const double* UL, const double* UR,
+                     double pL, double pR, double* uL, double* uR) {
+  const int nv = dim + 2;
+  const double cL = sound(gamma, pL, UL[0]), cR = sound(gamma, pR, UR[0]);
+  const double HL = (UL[nv - 1] + pL) / UL[0], HR = (UR[nv - 1] + pR) / UR[0];
+  const double sl = std::sqrt(UL[0]), sr = std::sqrt(UR[0]);
+  const double den = sl + sr;
+  double roe[3] = {0, 0, 0};
+  for (int m = 0; m < dim; ++m) roe[m] = fma(sl, uL[m], sr * uR[m]) / den;
+  const double Hroe = fma(sl, HL, sr * HR) / den;
+  double q2 = roe[0] * roe[0];
+  q2 = fma(roe[1], roe[1], q2);
+  if (dim == 3) q2 = fma(roe[2], roe[2], q2);
+  const double c2 = gm1 * (Hroe - 0.5 * q2);
+  const double croe = std::sqrt(std::fmax(c2, 0.0));
+  Speeds s;
+  s.sl = std::fmin(uL[d] - cL, roe[d] - croe);
+  s.sr = std::fmax(uR[d] + cR, roe[d] + croe);
+  return s;
+}
+
+void riemann(const Consts& k, int d, const double* UL, const double* UR, double* F,
+             double* speeds = nullptr) {
+  const int dim = k.dim, nv = k.nv;
+  double uL[3] = {0, 0, 0}, uR[3] = {0, 0, 0};
+  for (int m = 0; m < dim; ++m) {
+    uL[m] = UL[1 + m] / UL[0];
+    uR[m] = UR[1 + m] / UR[0];
+  }
+  const double pL = pressure(dim, UL, k.gm1), pR = pressure(dim, UR, k.gm1);
+  const Speeds S = batten(dim, k.gamma, k.gm1, d, UL, UR, pL, pR, uL, uR);
+  double FL[5], FR[5];
+  exact_flux(dim, d, UL, uL[d], pL, FL);
+  exact_flux(dim, d, UR, uR[d], pR, FR);
+  const double aL = UL[0] * (S.sl - uL[d]);
+  const double aR = UR[0] * (S.sr - uR[d]);
+  double sstar = 0.0;
+  {
+    double num = fma(aL, uL[d], pR - pL);
+    num = fma(-aR, uR[d], num);
+    sstar = num / (aL - aR);
+  }
+  if (speeds) {
+    speeds[0] = S.sl;
+    speeds[1] = S.sr;
+    speeds[2] = sstar;
+  }
+  if (S.sl >= 0.0) {
+    for (int v = 0; v < nv; ++v) F[v] = FL[v];
+    return;
+  }
+  if (S.sr <= 0.0) {
+    for (int v = 0; v < nv; ++v) F[v] = FR[v];
+    return;
+  }
+  if (k.riemann == KFVM_RIEMANN_HLL) {
+    const double ssr = S.sl * S.sr;
+    const double den = S.sr - S.sl;
+    for (int v = 0; v < nv; ++v) {
+      double t = S.sr * FL[v];
+      t = fma(-S.sl, FR[v], t);
+      t = fma(ssr, UR[v] - UL[v], t);
+      F[v] = t / den;
+    }
+    return;
+  }
+  // HLLC
+  const bool left = sstar >= 0.0;
+  const double* UK = left ? UL : UR;
+  const double* FK = left ? FL : FR;
+  const double* uK = left ? uL : uR;
+  const double SK = left ? S.sl : S.sr;
+  const double aK = left ? aL : aR;
+  const double pK = left ? pL : pR;
+  const double fac = aK / (SK - sstar);
+  double Us[5];
+  Us[0] = fac;
+  for (int m = 0; m < dim; ++m) Us[1 + m] = fac * (m == d ? sstar : uK[m]);
+  const double e = fma(sstar - uK[d], sstar + pK / aK, UK[nv - 1] / UK[0]);
+  Us[nv - 1] = fac * e;
+  for (int v = 0; v < nv; ++v) F[v] = fma(SK, Us[v] - UK[v], FK[v]);
+}
+
+// ------------------------------------------------------------- grid / slab
+inline int wrap(int i, int n, int bc) {
+  if (bc == KFVM_BC_PERIODIC) return ((i % n) + n) % n;
+  return i < 0 ? 0 : (i >= n ? n - 1 : i);
+}
+
+// A slab of planes [p0, p0+np) along the slab axis sa = dim-1, stored with H
+// halo planes on each side; the other axes are remapped by the BC.
+struct Slab {
+  const Consts* k;
+  int sa, p0, np, H;
+  int ext[3];  // local extents (slab axis includes halos)
+  std::vector<double> U;
+
+  void init(const Consts& kk, int p0_, int np_) {
+    k = &kk;
+    sa = kk.dim - 1;
+    p0 = p0_;
+    np = np_;
+    H = kk.R + 1;
+    for (int a = 0; a < 3; ++a) ext[a] = kk.n[a];
+    ext[sa] = np + 2 * H;
+    U.assign((size_t)ext[0] * ext[1] * ext[2] * kk.nv, 0.0);
+  }
+  // global coords (i,j,k); slab axis must lie within [p0-H, p0+np+H)
+  inline const double* at(int i, int j, int kk) const {
+    int c[3] = {i, j, kk};
+    for (int a = 0; a < k->dim; ++a) {
+      if (a == sa)
+        c[a] = c[a] - (p0 - H);
+      else
+        c[a] = wrap(c[a], k->n[a], k->bc);
+    }
+    return U.data() + (((size_t)c[2] * ext[1] + c[1]) * ext[0] + c[0]) * k->nv;
+  }
+  // fill from a global AoS array: interior planes + halos (wrap/clamp of the
+  // global slab-axis index) — the in-memory halo exchange.
+  void load(const double* G) {
+    const int nsa = k->n[sa];
+    const size_t plane = (size_t)k->nv * (sa == 2 ? (size_t)k->n[0] * k->n[1] : (size_t)k->n[0]);
+    for (int lp = 0; lp < ext[sa]; ++lp) {
+      const int gp = wrap(p0 - H + lp, nsa, k->bc);
+      std::memcpy(U.data() + (size_t)lp * plane, G + (size_t)gp * plane, plane * sizeof(double));
+    }
+  }
+};
+
+// Contiguous slab split: the first n % P slabs get one extra plane.
+void slab_range(int n, int P, int r, int* p0, int* np) {
+  const int base = n / P, rem = n % P;
+  *np = base + (r < rem ? 1 : 0);
+  *p0 = r * base + (r < rem ? r : rem);
+}
+
+template <class F>
+void parallel_for(int n, int nthreads, F&& f) {
+  if (nthreads <= 1 || n < 2) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<int> next(0);
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t)
+    th.emplace_back([&]() {
+      for (int i; (i = next.fetch_add(1)) < n;) f(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+// Face states of one cell (global coords), after WENO-AO + positivity.
+int cell_states(const kfvm_table* t, const Consts& k, const Slab& S, int i, int j, int kk,
+                double* st /* [npts][nv] */) {
+  const int dim = k.dim, nv = k.nv, N0 = t->n_full, np = t->n_points;
+  const double* Uc = S.at(i, j, kk);
+  const Transform T = make_transform(dim, Uc);
+  std::vector<const double*> cells(N0);
+  for (int h = 0; h < N0; ++h)
+    cells[h] = S.at(i + t->offsets[3 * h], j + t->offsets[3 * h + 1], kk + t->offsets[3 * h + 2]);
+  double g[128], vals[64];
+  double W[64 * 5];
+  for (int v = 0; v < nv; ++v) {
+    for (int h = 0; h < N0; ++h) g[h] = to_recon(dim, T, k.gm1, cells[h], v);
+    weno_field(t, k, g, nullptr, nullptr, vals);
+    for (int s = 0; s < np; ++s) W[s * nv + v] = vals[s];
+  }
+  for (int s = 0; s < np; ++s) from_recon(dim, T, k.inv_gm1, W + s * nv, st + s * nv);
+  double nbr[27 * 5];
+  const int kr = dim == 3 ? 1 : 0;
+  int m = 0;
+  for (int c = -kr; c <= kr; ++c)
+    for (int b = -1; b <= 1; ++b)
+      for (int a = -1; a <= 1; ++a, ++m) std::memcpy(nbr + m * nv, S.at(i + a, j + b, kk + c), nv * sizeof(double));
+  return limit_cell(k, np, st, nbr, nullptr);
+}
+
+// RHS over the slab's interior planes.  out: AoS [np planes]
+int slab_rhs(const kfvm_table* t, const Consts& k, const Slab& S, double* out, int nthreads,
+             double* states_out = nullptr) {
+  const int dim = k.dim, nv = k.nv, npts = t->n_points;
+  const int rp = npts / (2 * dim);
+  // extended-cell box: [-1, n] in every axis, slab axis [p0-1, p0+np]
+  int lo[3], cnt[3];
+  for (int a = 0; a < 3; ++a) {
+    if (a >= dim) {
+      lo[a] = 0;
+      cnt[a] = 1;
+    } else if (a == S.sa) {
+      lo[a] = S.p0 - 1;
+      cnt[a] = S.np + 2;
+    } else {
+      lo[a] = -1;
+      cnt[a] = k.n[a] + 2;
+    }
+  }
+  const size_t ncell = (size_t)cnt[0] * cnt[1] * cnt[2];
+  const size_t cs = (size_t)npts * nv;
+  std::vector<double> st(ncell * cs);
+  std::atomic<int> err(0);
+  const int nrows = cnt[1] * cnt[2];
+  parallel_for(nrows, nthreads, [&](int row) {
+    const int b = row % cnt[1], c = row / cnt[1];
+    for (int a = 0; a < cnt[0]; ++a) {
+      const size_t id = ((size_t)c * cnt[1] + b) * cnt[0] + a;
+      const int e = cell_states(t, k, S, lo[0] + a, lo[1] + b, lo[2] + c, st.data() + id * cs);
+      if (e) err.store(e);
+    }
+  });
+  if (err.load()) return err.load();
+  auto sid = [&](int i, int j, int kk) {
+    return (((size_t)(kk - lo[2]) * cnt[1] + (j - lo[1])) * cnt[0] + (i - lo[0])) * cs;
+  };
+  if (states_out) {  // interior cells of the slab, [cell][point][var]
+    size_t o = 0;
+    const int kn = dim == 3 ? k.n[2] : 1;
+    for (int c = 0; c < kn; ++c)
+      for (int b = 0; b < k.n[1]; ++b)
+        for (int a = 0; a < k.n[0]; ++a) {
+          const int cc[3] = {a, b, c};
+          if (cc[S.sa] < S.p0 || cc[S.sa] >= S.p0 + S.np) continue;
+          std::memcpy(states_out + o, st.data() + sid(a, b, c), cs * sizeof(double));
+          o += cs;
+        }
+  }
+  // face-averaged fluxes and the divergence
+  int ilo[3] = {0, 0, 0}, icnt[3] = {k.n[0], k.n[1], dim == 3 ? k.n[2] : 1};
+  ilo[S.sa] = S.p0;
+  icnt[S.sa] = S.np;
+  const double* fw = t->face_weights;
+  auto face_flux = [&](int d, int i, int j, int kk, double* Fbar) {
+    // face between cell (i,j,kk)-e_d (left) and (i,j,kk) (right)
+    int li = i, lj = j, lk = kk;
+    if (d == 0) li--;
+    if (d == 1) lj--;
+    if (d == 2) lk--;
+    const double* SL = st.data() + sid(li, lj, lk);
+    const double* SR = st.data() + sid(i, j, kk);
+    for (int v = 0; v < nv; ++v) Fbar[v] = 0.0;
+    double F[5];
+    for (int m = 0; m < rp; ++m) {
+      const int sL = (2 * d + 1) * rp + m;  // +d face of the left cell
+      const int sR = (2 * d) * rp + m;      // -d face of the right cell
+      riemann(k, d, SL + sL * nv, SR + sR * nv, F);
+      for (int v = 0; v < nv; ++v) Fbar[v] = fma(fw[sR], F[v], Fbar[v]);
+    }
+  };
+  const int irows = icnt[1] * icnt[2];
+  parallel_for(irows, nthreads, [&](int row) {
+    const int j = ilo[1] + row % icnt[1], kk = ilo[2] + row / icnt[1];
+    double Flo[3][5], Fhi[3][5];
+    for (int i = 0; i < icnt[0]; ++i) {
+      for (int d = 0; d < dim; ++d) {
+        face_flux(d, i, j, kk, Flo[d]);
+        face_flux(d, i + (d == 0), j + (d == 1), kk + (d == 2), Fhi[d]);
+      }
+      double* o = out + ((((size_t)(kk - ilo[2]) * icnt[1] + (j - ilo[1])) * icnt[0]) + i) * nv;
+      for (int v = 0; v < nv; ++v) {
+        double acc = Fhi[0][v] - Flo[0][v];
+        acc = acc + (Fhi[1][v] - Flo[1][v]);
+        if (dim == 3) acc = acc + (Fhi[2][v] - Flo[2][v]);
+        o[v] = -(acc / k.dx);
+      }
+    }
+  });
+  return 0;
+}
+
+double cell_speed(const Consts& k, const double* U) {  // S:610 (+|w|+c in 3-D)
+  const double p = pressure(k.dim, U, k.gm1);
+  const double c = sound(k.gamma, p, U[0]);
+  double s = std::fabs(U[1] / U[0]) + c;
+  s = s + (std::fabs(U[2] / U[0]) + c);
+  if (k.dim == 3) s = s + (std::fabs(U[3] / U[0]) + c);
+  return s;
+}
+
+bool admissible(const Consts& k, const double* U) {
+  return U[0] > 0.0 && pressure(k.dim, U, k.gm1) > 0.0 && std::isfinite(U[k.nv - 1]);
+}
+
+size_t ncells(const Consts& k) { return (size_t)k.n[0] * k.n[1] * k.n[2]; }
+
+// stage combine (pinned)
+inline double combine(int stage, double u0, double uk, double L, double dt) {
+  // Shu-Osher SSP-RK3 in increment form: u_{k+1} = u0 + b_k (w - u0) with
+  // w = u_k + dt L(u_k), b = 1, 1/4, 2/3 (exact free-stream preservation)
+  const double w = fma(dt, L, uk);
+  if (stage == 1) return w;
+  if (stage == 2) return fma(0.25, w - u0, u0);
+  return fma(2.0 / 3.0, w - u0, u0);
+}
+
+int full_rhs(const kfvm_table* t, const Consts& k, const double* U, double* out, int nslabs,
+             int nthreads) {
+  const int sa = k.dim - 1;
+  const size_t plane = ncells(k) / k.n[sa] * k.nv;
+  for (int r = 0; r < nslabs; ++r) {
+    int p0, np;
+    slab_range(k.n[sa], nslabs, r, &p0, &np);
+    Slab S;
+    S.init(k, p0, np);
+    S.load(U);
+    const int e = slab_rhs(t, k, S, out + (size_t)p0 * plane, nthreads);
+    if (e) return e;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kfo_rhs(const kfvm_config* cfg, const kfvm_table* t, const double* U, double* dUdt,
+            int nthreads) {
+  const Consts k = make_consts(cfg, t);
+  return full_rhs(t, k, U, dUdt, 1, nthreads);
+}
+
+int kfo_states(const kfvm_config* cfg, const kfvm_table* t, const double* U, double* states,
+               int nthreads) {
+  const Consts k = make_consts(cfg, t);
+  Slab S;
+  S.init(k, 0, k.n[k.dim - 1]);
+  S.load(U);
+  std::vector<double> tmp(ncells(k) * k.nv);
+  return slab_rhs(t, k, S, tmp.data(), nthreads, states);
+}
+
+int kfo_select_dt(const kfvm_config* cfg, const double* U, double* dt) {
+  const Consts k = make_consts(cfg, nullptr);
+  double smax = 0.0;
+  for (size_t c = 0; c < ncells(k); ++c) smax = std::fmax(smax, cell_speed(k, U + c * k.nv));
+  *dt = (k.cfl * k.dx) / smax;
+  return std::isfinite(*dt) && *dt > 0 ? 0 : 2;
+}
+
+int kfo_stage(const kfvm_config* cfg, const kfvm_table* t, const double* U0, const double* Uk,
+              double* Uout, int stage, double dt, int nthreads) {
+  const Consts k = make_consts(cfg, t);
+  const size_t n = ncells(k) * k.nv;
+  std::vector<double> L(n);
+  const int e = full_rhs(t, k, Uk, L.data(), 1, nthreads);
+  if (e) return e;
+  for (size_t i = 0; i < n; ++i) Uout[i] = combine(stage, U0[i], Uk[i], L[i], dt);
+  for (size_t c = 0; c < ncells(k); ++c)
+    if (!admissible(k, Uout + c * k.nv)) return 2;
+  return 0;
+}
+
+int kfo_run(const kfvm_config* cfg, const kfvm_table* t, double* U, int nsteps, double* dt_seq,
+            int nslabs, int nthreads) {
+  const Consts k = make_consts(cfg, t);
+  const size_t n = ncells(k) * k.nv;
+  std::vector<double> U0(n), Uk(n), L(n);
+  for (int step = 0; step < nsteps; ++step) {
+    double dt;
+    if (kfo_select_dt(cfg, U, &dt)) return 2;
+    if (dt_seq) dt_seq[step] = dt;
+    std::memcpy(U0.data(), U, n * sizeof(double));
+    for (int stage = 1; stage <= 3; ++stage) {
+      const double* src = stage == 1 ? U0.data() : U;
+      const int e = full_rhs(t, k, src, L.data(), nslabs, nthreads);
+      if (e) return e;
+      for (size_t i = 0; i < n; ++i) Uk[i] = combine(stage, U0[i], src[i], L[i], dt);
+      std::memcpy(U, Uk.data(), n * sizeof(double));
+      for (size_t c = 0; c < ncells(k); ++c)
+        if (!admissible(k, U + c * k.nv)) return 2;
+    }
+  }
+  return 0;
+}
+
+int kfo_sample_stage(const kfvm_config* cfg, const kfvm_table* t, const double* U, int p0, int np,
+                     int nthreads, double* seconds) {
+  const Consts k = make_consts(cfg, t);
+  Slab S;
+  S.init(k, p0, np);
+  S.load(U);
+  std::vector<double> out(ncells(k) / k.n[k.dim - 1] * np * k.nv), un(out.size());
+  const auto t0 = std::chrono::steady_clock::now();
+  const int e = slab_rhs(t, k, S, out.data(), nthreads);
+  // the stage-1 combine u1 = u + dt L(u) is part of the unit of work
+  const size_t plane = out.size() / np;
+  const double* Ui = U + (size_t)p0 * plane;
+  for (size_t i = 0; i < out.size(); ++i) un[i] = combine(1, Ui[i], Ui[i], out[i], 1e-3);
+  *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return e;
+}
+
+double kfo_pressure(int dim, const double* U, double gamma) { return pressure(dim, U, gamma - 1.0); }
+
+double kfo_sound_speed(int dim, const double* U, double gamma) {
+  return sound(gamma, pressure(dim, U, gamma - 1.0), U[0]);
+}
+
+void kfo_transform(int dim, const double* Uref, double gamma, double* phi, double* phi_inv) {
+  const int nv = dim + 2;
+  const Transform T = make_transform(dim, Uref);
+  const double gm1 = gamma - 1.0, inv_gm1 = 1.0 / gm1;
+  for (int c = 0; c < nv; ++c) {
+    double e[5] = {0, 0, 0, 0, 0}, w[5], u[5];
+    e[c] = 1.0;
+    for (int v = 0; v < nv; ++v) w[v] = to_recon(dim, T, gm1, e, v);
+    // column c of Phi (resp. Phi^-1) is the image of the unit vector e_c
+    for (int v = 0; v < nv; ++v) phi[v * nv + c] = w[v];
+    from_recon(dim, T, inv_gm1, e, u);
+    for (int v = 0; v < nv; ++v) phi_inv[v * nv + c] = u[v];
+  }
+}
+
+void kfo_to_recon(int dim, const double* Uref, double gamma, const double* U, double* W) {
+  const Transform T = make_transform(dim, Uref);
+  for (int v = 0; v < dim + 2; ++v) W[v] = to_recon(dim, T, gamma - 1.0, U, v);
+}
+
+void kfo_from_recon(int dim, const double* Uref, double gamma, const double* W, double* U) {
+  const Transform T = make_transform(dim, Uref);
+  from_recon(dim, T, 1.0 / (gamma - 1.0), W, U);
+}
+
+void kfo_riemann(int dim, int solver, int axis, const double* UL, const double* UR, double gamma,
+                 double* F) {
+  kfvm_config c{};
+  c.dim = dim;
+  c.gamma = gamma;
+  c.riemann = solver;
+  c.dx = 1.0;
+  c.nx = c.ny = c.nz = 1;
+  Consts k = make_consts(&c, nullptr);
+  riemann(k, axis, UL, UR, F);
+}
+
+void kfo_wavespeeds(int dim, int axis, const double* UL, const double* UR, double gamma,
+                    double* out) {
+  kfvm_config c{};
+  c.dim = dim;
+  c.gamma = gamma;
+  c.dx = 1.0;
+  c.nx = c.ny = c.nz = 1;
+  Consts k = make_consts(&c, nullptr);
+  double F[5];
+  riemann(k, axis, UL, UR, F, out);
+}
+
+void kfo_exact_flux(int dim, int axis, const double* U, double gamma, double* F) {
+  const double p = pressure(dim, U, gamma - 1.0);
+  exact_flux(dim, axis, U, U[1 + axis] / U[0], p, F);
+}
+
+void kfo_weno(const kfvm_table* t, double dx, double eps, const double* g, double* beta,
+              double* omega, double* values) {
+  kfvm_config c{};
+  c.dim = t->dim;
+  c.radius = t->radius;
+  c.dx = dx;
+  c.eps = eps;
+  c.gamma = 1.4;
+  c.nx = c.ny = c.nz = 1;
+  const Consts k = make_consts(&c, t);
+  weno_field(t, k, g, beta, omega, values);
+}
+
+int kfo_limit(int dim, int n, double* states, const double* nbr, double gamma, double kappa,
+              double kf, double* info) {
+  kfvm_config c{};
+  c.dim = dim;
+  c.gamma = gamma;
+  c.kappa = kappa;
+  c.flattener_kf = kf;
+  c.dx = 1.0;
+  c.nx = c.ny = c.nz = 1;
+  const Consts k = make_consts(&c, nullptr);
+  return limit_cell(k, n, states, nbr, info);
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+/*
+ * kfvm_oracle.h — CPU oracle of the KFVM-WENO FP64 stage update.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This is a plain C++ restatement of the
+ * reference algorithm (SPEC.md modules weno S:241-300, euler_state
+ * S:302-384, limiters/positivity S:410-446, riemann S:466-519, solver
+ * S:521-645; §3-§5 for 3-D) used as the parity checker by tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg.
+ * The product (paper_2401_16543_b200/) never links or calls it.
+ *
+ * Parity: the reference tree ships no tests, fixtures or golden vectors for
+ * this path and does not build; the oracle is pinned by
+ * the SPEC's inline known-answer examples and invariants (tests/golden/
+ * spec_examples.json, tests/test_oracle_*.py) and by PAPER.md Table 1 EOCs.
+ */
+#ifndef KFVM_ORACLE_H_
+#define KFVM_ORACLE_H_
+
+#include "../include/kfvm_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Whole-grid operations on AoS interior state (reference layout). */
+int kfo_rhs(const kfvm_config* cfg, const kfvm_table* t, const double* U,
+            double* dUdt, int nthreads);
+int kfo_states(const kfvm_config* cfg, const kfvm_table* t, const double* U,
+               double* states, int nthreads);
+int kfo_select_dt(const kfvm_config* cfg, const double* U, double* dt);
+int kfo_stage(const kfvm_config* cfg, const kfvm_table* t, const double* U0,
+              const double* Uk, double* Uout, int stage, double dt, int nthreads);
+/* nsteps SSP-RK3 steps in place; dt_seq may be NULL.  nslabs > 1 runs the
+ * virtual slab decomposition (halo copies between slabs) of SURVEY §4(iii). */
+int kfo_run(const kfvm_config* cfg, const kfvm_table* t, double* U, int nsteps,
+            double* dt_seq, int nslabs, int nthreads);
+/* Same, restricted to the planes [p0, p0+np) of the slab axis of a bigger
+ * global grid: one RHS (stage-1 update) of the sub-box, for timing samples. */
+int kfo_sample_stage(const kfvm_config* cfg, const kfvm_table* t, const double* U,
+                     int p0, int np, int nthreads, double* seconds);
+
+/* Point functions (unit tests against the SPEC examples). */
+double kfo_pressure(int dim, const double* U, double gamma);
+double kfo_sound_speed(int dim, const double* U, double gamma);
+void kfo_transform(int dim, const double* Uref, double gamma, double* phi,
+                   double* phi_inv);
+void kfo_to_recon(int dim, const double* Uref, double gamma, const double* U,
+                  double* W);
+void kfo_from_recon(int dim, const double* Uref, double gamma, const double* W,
+                    double* U);
+void kfo_riemann(int dim, int solver, int axis, const double* UL,
+                 const double* UR, double gamma, double* F);
+void kfo_wavespeeds(int dim, int axis, const double* UL, const double* UR,
+                    double gamma, double* sl_sr_sstar);
+void kfo_exact_flux(int dim, int axis, const double* U, double gamma, double* F);
+/* beta/omega/WENO-AO for one scalar field on S0 (g has n_full entries). */
+void kfo_weno(const kfvm_table* t, double dx, double eps, const double* g,
+              double* beta, double* omega, double* values);
+/* Positivity limiter on n states of one cell; nbr holds the 3^dim
+ * neighbourhood averages (i fastest), nbr[(3^dim)/2] is the cell itself. */
+int kfo_limit(int dim, int n, double* states, const double* nbr, double gamma,
+              double kappa, double kf, double* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,151 @@
+"""Run configuration and the BASELINE.json workloads.
+
+GridConfig mirrors the solver subset of RunConfig and maps
+onto ``kfvm_config`` in include/kfvm_b200.h.  BASELINE_CONFIGS pins the five
+BASELINE.json configs; their IC recipes are completed by the pinned choices
+documented in DESIGN.md §6 (seeds below, splitmix64, max|s| over every GL
+point of the global grid, minimum-image sphere).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _abi
+
+
+@dataclass(frozen=True)
+class GridConfig:
+    dim: int = 2
+    radius: int = 2
+    nx: int = 64
+    ny: int = 64
+    nz: int = 1
+    bc: str = "periodic"        # "periodic" | "outflow"
+    riemann: str = "hllc"       # "hllc" | "hll"   (riemann.solver)
+    dx: float | None = None     # defaults to 1/nx (unit domain)
+    gamma: float = 1.4
+    cfl: float = 1.0            # S:728 default
+    eps: float = 1e-40
+    kappa: float = 0.4          # limiter.kappa
+    flattener_kf: float = 0.33  # limiter.flattener_kf
+    ell_over_delta: float = 5.0
+
+    def __post_init__(self):
+        if self.dim not in (2, 3):
+            raise ValueError("dim must be 2 or 3")
+        if self.radius not in (2, 3):
+            raise ValueError("unsupported stencil radius (must be 2 or 3)")
+        if self.bc not in ("periodic", "outflow"):
+            raise ValueError("bc must be periodic or outflow")
+        if self.riemann not in ("hllc", "hll"):
+            raise ValueError("riemann must be hllc or hll")
+        if min(self.nx, self.ny, self.nz) < 1:
+            raise ValueError("grid extents must be positive")
+
+    @property
+    def nvar(self) -> int:
+        return self.dim + 2
+
+    @property
+    def ncells(self) -> int:
+        return self.nx * self.ny * (self.nz if self.dim == 3 else 1)
+
+    @property
+    def shape(self) -> tuple:
+        return (self.nz, self.ny, self.nx) if self.dim == 3 else (self.ny, self.nx)
+
+    @property
+    def slab_extent(self) -> int:
+        return self.nz if self.dim == 3 else self.ny
+
+    def c_config(self) -> _abi.KfvmConfig:
+        c = _abi.KfvmConfig()
+        c.dim, c.radius = self.dim, self.radius
+        c.nx, c.ny, c.nz = self.nx, self.ny, (self.nz if self.dim == 3 else 1)
+        c.bc = _abi.BC_PERIODIC if self.bc == "periodic" else _abi.BC_OUTFLOW
+        c.riemann = _abi.RIEMANN_HLLC if self.riemann == "hllc" else _abi.RIEMANN_HLL
+        c.dx = float(self.dx if self.dx is not None else 1.0 / self.nx)
+        c.gamma, c.cfl, c.eps = self.gamma, self.cfl, self.eps
+        c.kappa, c.flattener_kf = self.kappa, self.flattener_kf
+        return c
+
+
+@dataclass(frozen=True)
+class ICSpec:
+    kind: str                 # fourier | voronoi | fourier_sphere | uniform | vortex | density_wave
+    seed: int = 0
+    n_modes: int = 8
+    n_regions: int = 16
+    origin: tuple = (0.0, 0.0, 0.0)
+    value: tuple = (1.0, 0.0, 0.0, 0.0, 1.0)
+
+    def c_params(self) -> _abi.KfvmIcParams:
+        kinds = {"fourier": _abi.IC_FOURIER, "voronoi": _abi.IC_VORONOI,
+                 "fourier_sphere": _abi.IC_FOURIER_SPHERE, "uniform": _abi.IC_UNIFORM,
+                 "vortex": _abi.IC_VORTEX, "density_wave": _abi.IC_DENSITY_WAVE}
+        p = _abi.KfvmIcParams()
+        p.kind = kinds[self.kind]
+        p.n_modes, p.n_regions, p.seed = self.n_modes, self.n_regions, self.seed
+        for i in range(3):
+            p.origin[i] = float(self.origin[i])
+        for i in range(5):
+            p.value[i] = float(self.value[i])
+        return p
+
+
+@dataclass(frozen=True)
+class Workload:
+    index: int
+    grid: GridConfig
+    ic: ICSpec
+    steps: int
+    text: str = ""
+
+
+def _wl(index, dim, n, bc, radius, cfl, steps, ic):
+    g = GridConfig(dim=dim, radius=radius, nx=n, ny=n, nz=(n if dim == 3 else 1), bc=bc, cfl=cfl)
+    return Workload(index, g, ic, steps)
+
+
+# BASELINE.json "configs" (1-based index as in SURVEY.md §8(d))
+BASELINE_CONFIGS = {
+    1: _wl(1, 2, 256, "periodic", 2, 0.4, 20, ICSpec("fourier", seed=0x5EED0001, n_modes=8)),
+    2: _wl(2, 2, 1024, "outflow", 2, 0.4, 50, ICSpec("voronoi", seed=0x5EED0002, n_regions=16)),
+    3: _wl(3, 3, 256, "periodic", 2, 0.3, 10, ICSpec("fourier", seed=0x5EED0003, n_modes=12)),
+    4: _wl(4, 3, 512, "outflow", 2, 0.3, 10, ICSpec("voronoi", seed=0x5EED0004, n_regions=64)),
+    5: _wl(5, 3, 1024, "periodic", 3, 0.3, 5, ICSpec("fourier_sphere", seed=0x5EED0005, n_modes=12)),
+}
+
+
+def baseline_config(index: int, n: int | None = None, nz: int | None = None) -> Workload:
+    """Config `index` of BASELINE.json, optionally at a reduced resolution n
+    (same recipe, same seed; used for parity cases and CPU samples)."""
+    w = BASELINE_CONFIGS[index]
+    if n is None and nz is None:
+        return w
+    g = w.grid
+    n = n or g.nx
+    nzz = nz if nz is not None else (n if g.dim == 3 else 1)
+    return replace(w, grid=replace(g, nx=n, ny=n, nz=nzz, dx=1.0 / n))
+
+
+def initial_condition(grid: GridConfig, ic: ICSpec, z0: int = 0, nz_local: int | None = None,
+                      nthreads: int | None = None) -> np.ndarray:
+    """Cell averages (AoS, shape grid.shape + (nvar,)) of the seeded IC on the
+    slab-axis planes [z0, z0+nz_local)."""
+    L = _abi.lib()
+    nzl = grid.slab_extent - z0 if nz_local is None else nz_local
+    plane = grid.nx * (grid.ny if grid.dim == 3 else 1)
+    U = np.empty(plane * nzl * grid.nvar, dtype=np.float64)
+    cfg = grid.c_config()
+    p = ic.c_params()
+    nt = nthreads or min(32, os.cpu_count() or 1)
+    rc = L.kfvm_ic_generate(C.byref(cfg), C.byref(p), z0, nzl, nt, U.ctypes.data)
+    if rc:
+        raise ValueError(f"kfvm_ic_generate failed with code {rc}")
+    shp = ((nzl, grid.ny, grid.nx) if grid.dim == 3 else (nzl, grid.nx)) + (grid.nvar,)
+    return U.reshape(shp)

@@ -1,0 +1,1216 @@
+// kfvm_gpu.cu — B200 (sm_100a) FP64 KFVM-WENO stage update + C-ABI handle.
+//
+// Hot path (BASELINE.json north_star):
+//   k_states  : per extended cell — stencil gather, Phi, beta_q, omega_q,
+//               WENO-AO face values at every face GL point, Phi^-1,
+//               positivity limiter (reconstruct_states)
+//   k_flux    : per face — Riemann solve at the R^(d-1) face GL points and the
+//               face quadrature
+//   k_update  : per cell — flux divergence, SSP-RK3 combine, admissibility
+//               check, max-wavespeed reduction for the next dt
+// plus the slab-axis halo fill (fill_ghost S:553-561 / NCCL send-recv) and the
+// device-resident dt.  The translation unit is compiled with -fmad=false:
+// every fma below is explicit, matching the oracle's FP contract.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kfvm_b200.h"
+#include "kfvm_device.cuh"
+#include "kfvm_ic_eval.h"
+#include "kfvm_ic_host.h"
+
+namespace kfvm_b200 {
+
+__constant__ DevConsts c_k;
+__constant__ DevTable c_t;
+__constant__ int c_gather[512];
+
+struct Geo {
+  int nx, nm, np_loc, H;  // x extent, mid extent (1 in 2-D), local slab planes, halo
+  long long pstride;      // elements per slab-axis plane
+  long long vstride;      // elements per variable
+};
+
+struct Chunk {
+  int c0, C;              // first local plane and number of planes
+  int ex, em, ep;         // extended box extents (x, mid, planes)
+  long long next;         // extended cells
+  int fx, fm, fp;         // face box extents
+  long long nfb;          // face-box cells
+};
+
+__device__ __forceinline__ int remap(int i, int n, int bc) {
+  if (bc == KFVM_BC_PERIODIC) {
+    i %= n;
+    return i < 0 ? i + n : i;
+  }
+  return i < 0 ? 0 : (i >= n ? n - 1 : i);
+}
+
+template <int DIM>
+__device__ __forceinline__ long long uidx(const Geo& g, int x, int j, int p) {
+  long long o = (long long)(p + g.H) * g.pstride + remap(x, g.nx, c_k.bc);
+  if (DIM == 3) o += (long long)remap(j, g.nm, c_k.bc) * g.nx;
+  return o;
+}
+
+constexpr int full_size(int dim, int R) {
+  return dim == 2 ? (R == 2 ? 13 : 29) : (R == 2 ? 33 : 123);
+}
+constexpr int npoints(int dim, int R) { return dim == 2 ? 4 * R : 6 * R * R; }
+
+// ---------------------------------------------------------------- k_states
+template <int DIM, int R>
+__global__ void __launch_bounds__(128) k_states(const double* __restrict__ U,
+                                                double* __restrict__ St, Geo g, Chunk ch,
+                                                int* __restrict__ err) {
+  constexpr int nv = DIM + 2;
+  constexpr int N0 = full_size(DIM, R);
+  constexpr int NP = npoints(DIM, R);
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= ch.next) return;
+  const int a = (int)(tid % ch.ex);
+  const long long r1 = tid / ch.ex;
+  const int b = (int)(r1 % ch.em);
+  const int c = (int)(r1 / ch.em);
+  const int x = a - 1;
+  const int j = DIM == 3 ? b - 1 : 0;
+  const int p = ch.c0 - 1 + c;
+
+  double Uc[nv];
+  const long long ic = uidx<DIM>(g, x, j, p);
+#pragma unroll
+  for (int v = 0; v < nv; ++v) Uc[v] = U[v * g.vstride + ic];
+  const DTransform T = d_make_transform(DIM, Uc);
+
+  long long cell[N0];
+  for (int h = 0; h < N0; ++h)
+    cell[h] = uidx<DIM>(g, x + c_t.off_x[h], j + c_t.off_m[h], p + c_t.off_p[h]);
+
+  double W[NP * nv];
+  double gv[N0];
+  const int NS = c_t.n_stencils;
+  for (int v = 0; v < nv; ++v) {
+    for (int h = 0; h < N0; ++h) {
+      double Uh[nv];
+#pragma unroll
+      for (int u = 0; u < nv; ++u) Uh[u] = U[u * g.vstride + cell[h]];
+      gv[h] = d_to_recon(DIM, T, c_k.gm1, Uh, v);
+    }
+    double wt[8], cq[8];
+    for (int q = 0; q < NS; ++q) {
+      const int N = c_t.size[q];
+      const int* gat = c_gather + c_t.cell_offset[q];
+      const double* D = c_t.deriv + (long long)c_t.cell_offset[q] * c_t.n_alpha;
+      double beta = 0.0;
+      for (int al = 0; al < c_t.n_alpha; ++al) {
+        double d = 0.0;
+        for (int h = 0; h < N; ++h) d = fma(__ldg(D + al * N + h), gv[gat[h]], d);
+        beta = fma(c_t.scale[al], d * d, beta);
+      }
+      wt[q] = c_t.gamma_lin[q] / fma(beta, beta, c_k.eps);
+    }
+    double sum = wt[0];
+    for (int q = 1; q < NS; ++q) sum = sum + wt[q];
+    double om[8];
+    for (int q = 0; q < NS; ++q) om[q] = wt[q] / sum;
+    cq[0] = om[0] / c_t.gamma_lin[0];
+    for (int q = 1; q < NS; ++q) cq[q] = fma(-cq[0], c_t.gamma_lin[q], om[q]);
+    for (int s = 0; s < NP; ++s) {
+      double val = 0.0;
+      for (int q = 0; q < NS; ++q) {
+        const int N = c_t.size[q];
+        const int* gat = c_gather + c_t.cell_offset[q];
+        const double* rr = c_t.face + (long long)c_t.cell_offset[q] * NP + (long long)s * N;
+        double pp = 0.0;
+        for (int h = 0; h < N; ++h) pp = fma(__ldg(rr + h), gv[gat[h]], pp);
+        val = (q == 0) ? cq[0] * pp : fma(cq[q], pp, val);
+      }
+      W[s * nv + v] = val;
+    }
+  }
+  double st[NP * nv];
+  for (int s = 0; s < NP; ++s) d_from_recon(DIM, T, c_k.inv_gm1, W + s * nv, st + s * nv);
+  constexpr int NN = DIM == 3 ? 27 : 9;
+  double nbr[NN * nv];
+  {
+    int m = 0;
+    const int kr = DIM == 3 ? 1 : 0;
+    for (int cc = -1; cc <= 1; ++cc)
+      for (int bb = -kr; bb <= kr; ++bb)
+        for (int aa = -1; aa <= 1; ++aa, ++m) {
+          // neighbourhood order: i fastest, then mid (3-D) / slab (2-D), then slab
+          int jj = j, pp = p;
+          if (DIM == 3) {
+            jj = j + bb;
+            pp = p + cc;
+          } else {
+            pp = p + cc;
+          }
+          const long long o = uidx<DIM>(g, x + aa, jj, pp);
+#pragma unroll
+          for (int v = 0; v < nv; ++v) nbr[m * nv + v] = U[v * g.vstride + o];
+        }
+  }
+  if (d_limit<DIM>(c_k, NP, st, nbr)) atomicOr(err, 2);
+  for (int s = 0; s < NP; ++s)
+#pragma unroll
+    for (int v = 0; v < nv; ++v) St[(long long)(s * nv + v) * ch.next + tid] = st[s * nv + v];
+}
+
+// ------------------------------------------------------------------ k_flux
+template <int DIM>
+__device__ __forceinline__ long long sidx(const Chunk& ch, int x, int j, int p) {
+  // extended-cell index; p relative to the chunk's first plane
+  return ((long long)(p + 1) * ch.em + (DIM == 3 ? j + 1 : 0)) * ch.ex + (x + 1);
+}
+
+template <int DIM, int R>
+__global__ void __launch_bounds__(128) k_flux(const double* __restrict__ St,
+                                              double* __restrict__ F, Geo g, Chunk ch) {
+  constexpr int nv = DIM + 2;
+  constexpr int NP = npoints(DIM, R);
+  constexpr int RP = NP / (2 * DIM);
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= ch.nfb) return;
+  const int a = (int)(tid % ch.fx);
+  const long long r1 = tid / ch.fx;
+  const int b = (int)(r1 % ch.fm);
+  const int c = (int)(r1 / ch.fm);
+  const int nm = DIM == 3 ? g.nm : 1;
+  for (int d = 0; d < DIM; ++d) {
+    const bool slab = d == DIM - 1;
+    const bool mid = DIM == 3 && d == 1;
+    const bool valid = (d == 0 ? true : a < g.nx) && (mid ? true : (DIM == 3 ? b < nm : true)) &&
+                       (slab ? true : c < ch.C);
+    if (!valid) continue;
+    const int x = a, j = DIM == 3 ? b : 0, p = c;
+    const int lx = x - (d == 0), lj = j - (mid ? 1 : 0), lp = p - (slab ? 1 : 0);
+    const long long iL = sidx<DIM>(ch, lx, lj, lp);
+    const long long iR = sidx<DIM>(ch, x, j, p);
+    double Fb[nv];
+#pragma unroll
+    for (int v = 0; v < nv; ++v) Fb[v] = 0.0;
+    for (int m = 0; m < RP; ++m) {
+      const int sL = (2 * d + 1) * RP + m;
+      const int sR = (2 * d) * RP + m;
+      double UL[nv], UR[nv], Fp[nv];
+#pragma unroll
+      for (int v = 0; v < nv; ++v) {
+        UL[v] = St[(long long)(sL * nv + v) * ch.next + iL];
+        UR[v] = St[(long long)(sR * nv + v) * ch.next + iR];
+      }
+      d_riemann<DIM>(c_k, d, UL, UR, Fp);
+#pragma unroll
+      for (int v = 0; v < nv; ++v) Fb[v] = fma(c_t.face_w[sR], Fp[v], Fb[v]);
+    }
+#pragma unroll
+    for (int v = 0; v < nv; ++v) F[(long long)(d * nv + v) * ch.nfb + tid] = Fb[v];
+  }
+}
+
+// ---------------------------------------------------------------- k_update
+// mode 0: write L(u) into Uout; mode 1..3: SSP-RK3 stage combine.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_update(const double* __restrict__ F,
+                                                const double* __restrict__ U0,
+                                                const double* __restrict__ Uk,
+                                                double* __restrict__ Uout, Geo g, Chunk ch,
+                                                int stage, const double* __restrict__ dtp,
+                                                unsigned long long* __restrict__ smax,
+                                                int* __restrict__ err) {
+  constexpr int nv = DIM + 2;
+  const int nm = DIM == 3 ? g.nm : 1;
+  const long long ncell = (long long)g.nx * nm * ch.C;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= ncell) return;
+  const int a = (int)(tid % g.nx);
+  const long long r1 = tid / g.nx;
+  const int b = (int)(r1 % nm);
+  const int c = (int)(r1 / nm);
+  const long long f0 = ((long long)c * ch.fm + (DIM == 3 ? b : 0)) * ch.fx + a;
+  long long fh[3];
+  fh[0] = f0 + 1;
+  if (DIM == 3) {
+    fh[1] = f0 + ch.fx;
+    fh[2] = f0 + (long long)ch.fm * ch.fx;
+  } else {
+    fh[1] = f0 + (long long)ch.fm * ch.fx;
+  }
+  const long long ou = (long long)(ch.c0 + c + g.H) * g.pstride + (long long)b * g.nx + a;
+  const double dt = stage ? *dtp : 0.0;
+  double un[nv];
+#pragma unroll
+  for (int v = 0; v < nv; ++v) {
+    double acc = F[(long long)(0 * nv + v) * ch.nfb + fh[0]] - F[(long long)(0 * nv + v) * ch.nfb + f0];
+    acc = acc + (F[(long long)(1 * nv + v) * ch.nfb + fh[1]] - F[(long long)(1 * nv + v) * ch.nfb + f0]);
+    if (DIM == 3)
+      acc = acc + (F[(long long)(2 * nv + v) * ch.nfb + fh[2]] - F[(long long)(2 * nv + v) * ch.nfb + f0]);
+    const double L = -(acc / c_k.dx);
+    if (stage == 0) {
+      un[v] = L;
+    } else {
+      un[v] = d_combine(stage, U0[v * g.vstride + ou], Uk[v * g.vstride + ou], L, dt, c_k.c13,
+                        c_k.c23);
+    }
+    Uout[v * g.vstride + ou] = un[v];
+  }
+  if (stage) {
+    if (!d_admissible<DIM>(c_k, un)) atomicOr(err, 2);
+    if (stage == 3 && smax) {
+      const double s = d_cell_speed<DIM>(c_k, un);
+      if (s > 0.0) atomicMax(smax, (unsigned long long)__double_as_longlong(s));
+    }
+  }
+}
+
+template <int DIM>
+__global__ void k_speed(const double* __restrict__ U, Geo g, unsigned long long* smax) {
+  constexpr int nv = DIM + 2;
+  const int nm = DIM == 3 ? g.nm : 1;
+  const long long ncell = (long long)g.nx * nm * g.np_loc;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= ncell) return;
+  const long long ou = (long long)g.H * g.pstride + tid;
+  double u[nv];
+#pragma unroll
+  for (int v = 0; v < nv; ++v) u[v] = U[v * g.vstride + ou];
+  const double s = d_cell_speed<DIM>(c_k, u);
+  if (s > 0.0) atomicMax(smax, (unsigned long long)__double_as_longlong(s));
+}
+
+// dt = cfl*dx / smax on the device (select_dt)
+__global__ void k_dt(unsigned long long* smax, double* dt_cur, double* dt_seq, int* step,
+                     int cap, int* err) {
+  const double s = __longlong_as_double((long long)*smax);
+  const double dt = (c_k.cfl * c_k.dx) / s;
+  if (!(dt > 0.0) || !isfinite(dt)) atomicOr(err, 2);
+  *dt_cur = dt;
+  const int st = *step;
+  if (st < cap) dt_seq[st] = dt;
+  *step = st + 1;
+  *smax = 0ULL;
+}
+
+// slab-axis halo planes from the rank's own planes (1 rank: wrap/clamp; end
+// ranks with outflow: clamp).  which: bit0 = low side, bit1 = high side.
+__global__ void k_halo_local(double* __restrict__ U, Geo g, int nv, int nglob, int which) {
+  const long long per = (long long)g.H * g.pstride;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= 2 * per * nv) return;
+  const int side = (int)(tid / (per * nv));
+  if (!((which >> side) & 1)) return;
+  const long long r = tid % (per * nv);
+  const int v = (int)(r / per);
+  const long long e = r % per;
+  const int l = (int)(e / g.pstride);
+  const long long o = e % g.pstride;
+  int p, src;
+  if (side == 0) {
+    p = -g.H + l;
+  } else {
+    p = g.np_loc + l;
+  }
+  if (g.np_loc == nglob)
+    src = remap(p, nglob, c_k.bc);
+  else
+    src = p < 0 ? 0 : g.np_loc - 1;  // outflow clamp at a global end
+  U[v * g.vstride + (long long)(p + g.H) * g.pstride + o] =
+      U[v * g.vstride + (long long)(src + g.H) * g.pstride + o];
+}
+
+// AoS (host order) <-> SoA interior planes
+template <int DIR>
+__global__ void k_transpose(double* __restrict__ soa, double* __restrict__ aos, Geo g, int nv) {
+  const long long n = (long long)g.pstride * g.np_loc;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n * nv) return;
+  const long long c = tid / nv;
+  const int v = (int)(tid % nv);
+  const long long o = (long long)g.H * g.pstride + c;
+  if (DIR == 0)
+    soa[v * g.vstride + o] = aos[tid];
+  else
+    aos[tid] = soa[v * g.vstride + o];
+}
+
+// states of interior cells [cell][s][v] from the extended-box St
+template <int DIM>
+__global__ void k_extract_states(const double* __restrict__ St, double* __restrict__ out, Geo g,
+                                 Chunk ch, int NP) {
+  constexpr int nv = DIM + 2;
+  const int nm = DIM == 3 ? g.nm : 1;
+  const long long ncell = (long long)g.nx * nm * ch.C;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= ncell * NP * nv) return;
+  const long long cell = tid / (NP * nv);
+  const int sv = (int)(tid % (NP * nv));
+  const int a = (int)(cell % g.nx);
+  const long long r1 = cell / g.nx;
+  const int b = (int)(r1 % nm);
+  const int c = (int)(r1 / nm);
+  out[tid] = St[(long long)sv * ch.next + sidx<DIM>(ch, a, DIM == 3 ? b : 0, c)];
+}
+
+// GPU IC generator (same arithmetic as the host generator)
+__global__ void k_ic_norm(const ICPlan* P, int f, Geo g, int p0, unsigned long long* out) {
+  const int nm = P->dim == 3 ? g.nm : 1;
+  const long long n = (long long)g.nx * nm * P->n[P->dim - 1];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n) return;
+  const int i = (int)(tid % g.nx);
+  const long long r = tid / g.nx;
+  const int b = (int)(r % nm);
+  const int pl = (int)(r / nm);
+  const double m = P->dim == 3 ? cell_field_max(*P, P->f[f], i, b, pl)
+                               : cell_field_max(*P, P->f[f], i, pl, 0);
+  if (m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_ic_fill(const ICPlan* P, double* U, Geo g, int p0) {
+  const int nm = P->dim == 3 ? g.nm : 1;
+  const long long n = (long long)g.nx * nm * g.np_loc;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n) return;
+  const int i = (int)(tid % g.nx);
+  const long long r = tid / g.nx;
+  const int b = (int)(r % nm);
+  const int pl = (int)(r / nm);
+  double out[5];
+  if (P->dim == 3)
+    cell_average(*P, i, b, p0 + pl, out);
+  else
+    cell_average(*P, i, p0 + pl, 0, out);
+  const long long o = (long long)(pl + g.H) * g.pstride + (long long)b * g.nx + i;
+  for (int v = 0; v < P->dim + 2; ++v) U[v * g.vstride + o] = out[v];
+}
+
+}  // namespace kfvm_b200
+
+using namespace kfvm_b200;
+
+// ------------------------------------------------------------------- NCCL
+namespace {
+typedef struct {
+  char internal[128];
+} nccl_uid;
+typedef void* nccl_comm;
+struct NcclApi {
+  bool ok = false;
+  int (*GetUniqueId)(nccl_uid*);
+  int (*CommInitRank)(nccl_comm*, int, nccl_uid, int);
+  int (*CommDestroy)(nccl_comm);
+  int (*Send)(const void*, size_t, int, int, nccl_comm, cudaStream_t);
+  int (*Recv)(void*, size_t, int, int, nccl_comm, cudaStream_t);
+  int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
+  int (*GroupStart)();
+  int (*GroupEnd)();
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  const char* env = getenv("KFVM_NCCL_LIB");
+  void* h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.GetUniqueId = (int (*)(nccl_uid*))dlsym(h, "ncclGetUniqueId");
+  api.CommInitRank = (int (*)(nccl_comm*, int, nccl_uid, int))dlsym(h, "ncclCommInitRank");
+  api.CommDestroy = (int (*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+  api.Send = (int (*)(const void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclSend");
+  api.Recv = (int (*)(void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclRecv");
+  api.AllReduce = (int (*)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(
+      h, "ncclAllReduce");
+  api.GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
+  api.GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.AllReduce &&
+           api.GroupStart && api.GroupEnd && api.CommDestroy;
+  return api;
+}
+const int kNcclUint64 = 5;  // ncclUint64
+const int kNcclDouble = 8;  // ncclFloat64
+const int kNcclMax = 2;     // ncclMax
+}  // namespace
+
+struct kfvm_handle {
+  kfvm_config cfg{};
+  DevConsts kc{};
+  DevTable tab{};
+  std::vector<int> gather;
+  int dim = 0, R = 0, nv = 0, NP = 0;
+  int nsa = 0, p0 = 0, rank = 0, nranks = 1, device = 0;
+  Geo g{};
+  double *U0 = nullptr, *Ua = nullptr, *Ub = nullptr;
+  double *St = nullptr, *F = nullptr, *aos = nullptr;
+  size_t st_elems = 0, f_elems = 0, aos_elems = 0;
+  int chunk = 0;
+  int *d_gather = nullptr;
+  double *d_face = nullptr, *d_deriv = nullptr;
+  double *d_dt_seq = nullptr, *d_dt_cur = nullptr;
+  int dt_cap = 0;
+  unsigned long long* d_smax = nullptr;
+  int *d_step = nullptr, *d_err = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  bool timing = false;
+  cudaEvent_t ev[2];
+  double t_states = 0, t_flux = 0, t_update = 0, t_other = 0;
+  nccl_comm comm = nullptr;
+  long long launches = 0;
+  long long st_budget = 16LL << 30;
+  std::string err;
+};
+
+namespace {
+
+int fail(kfvm_handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(h, KFVM_ERR_DEVICE, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline unsigned blocks(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+Chunk make_chunk(const kfvm_handle* h, int c0, int C) {
+  Chunk ch;
+  ch.c0 = c0;
+  ch.C = C;
+  ch.ex = h->g.nx + 2;
+  ch.em = h->dim == 3 ? h->g.nm + 2 : 1;
+  ch.ep = C + 2;
+  ch.next = (long long)ch.ex * ch.em * ch.ep;
+  ch.fx = h->g.nx + 1;
+  ch.fm = h->dim == 3 ? h->g.nm + 1 : 1;
+  ch.fp = C + 1;
+  ch.nfb = (long long)ch.fx * ch.fm * ch.fp;
+  return ch;
+}
+
+void tic(kfvm_handle* h) {
+  if (h->timing) cudaEventRecord(h->ev[0], h->stream);
+}
+void toc(kfvm_handle* h, double* acc) {
+  if (!h->timing) return;
+  cudaEventRecord(h->ev[1], h->stream);
+  cudaEventSynchronize(h->ev[1]);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
+  *acc += ms;
+}
+
+template <int DIM, int R>
+void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
+  tic(h);
+  k_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->St, h->g, ch, h->d_err);
+  h->launches++;
+  toc(h, &h->t_states);
+  tic(h);
+  k_flux<DIM, R><<<blocks(ch.nfb, 128), 128, 0, h->stream>>>(h->St, h->F, h->g, ch);
+  h->launches++;
+  toc(h, &h->t_flux);
+}
+
+void states_and_flux(kfvm_handle* h, const double* U, const Chunk& ch) {
+  if (h->dim == 2 && h->R == 2) launch_states<2, 2>(h, U, ch);
+  if (h->dim == 2 && h->R == 3) launch_states<2, 3>(h, U, ch);
+  if (h->dim == 3 && h->R == 2) launch_states<3, 2>(h, U, ch);
+  if (h->dim == 3 && h->R == 3) launch_states<3, 3>(h, U, ch);
+}
+
+void update(kfvm_handle* h, const Chunk& ch, const double* U0, const double* Uk, double* Uout,
+            int stage) {
+  const long long n = (long long)h->g.nx * (h->dim == 3 ? h->g.nm : 1) * ch.C;
+  tic(h);
+  unsigned long long* sm = stage == 3 ? h->d_smax : nullptr;
+  if (h->dim == 2)
+    k_update<2><<<blocks(n, 256), 256, 0, h->stream>>>(h->F, U0, Uk, Uout, h->g, ch, stage,
+                                                       h->d_dt_cur, sm, h->d_err);
+  else
+    k_update<3><<<blocks(n, 256), 256, 0, h->stream>>>(h->F, U0, Uk, Uout, h->g, ch, stage,
+                                                       h->d_dt_cur, sm, h->d_err);
+  h->launches++;
+  toc(h, &h->t_update);
+}
+
+// fill the slab-axis halo planes of U (local copy and/or NCCL exchange)
+int halo(kfvm_handle* h, double* U) {
+  const long long per = (long long)h->g.H * h->g.pstride;
+  tic(h);
+  if (h->nranks == 1) {
+    k_halo_local<<<blocks(2 * per * h->nv, 256), 256, 0, h->stream>>>(U, h->g, h->nv, h->nsa, 3);
+    h->launches++;
+  } else {
+    NcclApi& N = nccl();
+    const bool periodic = h->cfg.bc == KFVM_BC_PERIODIC;
+    const int lo = h->rank - 1, hi = h->rank + 1;
+    const bool has_lo = periodic || lo >= 0, has_hi = periodic || hi < h->nranks;
+    const int plo = (lo + h->nranks) % h->nranks, phi = hi % h->nranks;
+    int which = (has_lo ? 0 : 1) | (has_hi ? 0 : 2);
+    if (which) {
+      k_halo_local<<<blocks(2 * per * h->nv, 256), 256, 0, h->stream>>>(U, h->g, h->nv, h->nsa,
+                                                                         which);
+      h->launches++;
+    }
+    // per peer pair the order is: upward transfer (my top interior -> the
+    // upper rank's bottom halo), then downward; this keeps send/recv matching
+    // correct when both neighbours are the same rank (2 ranks, periodic).
+    N.GroupStart();
+    for (int v = 0; v < h->nv; ++v) {
+      double* base = U + (long long)v * h->g.vstride;
+      double* top_int = base + (long long)h->g.np_loc * h->g.pstride;
+      double* top_halo = base + (long long)(h->g.np_loc + h->g.H) * h->g.pstride;
+      double* bot_int = base + per;
+      double* bot_halo = base;
+      if (has_hi) N.Send(top_int, per, kNcclDouble, phi, h->comm, h->stream);
+      if (has_lo) N.Recv(bot_halo, per, kNcclDouble, plo, h->comm, h->stream);
+      if (has_lo) N.Send(bot_int, per, kNcclDouble, plo, h->comm, h->stream);
+      if (has_hi) N.Recv(top_halo, per, kNcclDouble, phi, h->comm, h->stream);
+    }
+    if (N.GroupEnd() != 0) return fail(h, KFVM_ERR_DEVICE, "ncclGroupEnd failed");
+  }
+  toc(h, &h->t_other);
+  return KFVM_OK;
+}
+
+int reduce_smax(kfvm_handle* h) {
+  if (h->nranks == 1) return KFVM_OK;
+  // positive doubles order like their bit patterns: max on uint64 is exact
+  if (nccl().AllReduce(h->d_smax, h->d_smax, 1, kNcclUint64, kNcclMax, h->comm, h->stream) != 0)
+    return fail(h, KFVM_ERR_DEVICE, "ncclAllReduce failed");
+  return KFVM_OK;
+}
+
+// one stage: halo, then per chunk states -> flux -> update
+int run_stage(kfvm_handle* h, const double* Uin, double* Uout, int stage) {
+  int rc = halo(h, const_cast<double*>(Uin));
+  if (rc) return rc;
+  for (int c0 = 0; c0 < h->g.np_loc; c0 += h->chunk) {
+    const Chunk ch = make_chunk(h, c0, std::min(h->chunk, h->g.np_loc - c0));
+    states_and_flux(h, Uin, ch);
+    update(h, ch, h->U0, Uin, Uout, stage);
+  }
+  return KFVM_OK;
+}
+
+int enqueue_dt(kfvm_handle* h) {
+  int rc = reduce_smax(h);
+  if (rc) return rc;
+  tic(h);
+  k_dt<<<1, 1, 0, h->stream>>>(h->d_smax, h->d_dt_cur, h->d_dt_seq, h->d_step, h->dt_cap, h->d_err);
+  h->launches++;
+  toc(h, &h->t_other);
+  return KFVM_OK;
+}
+
+int enqueue_step(kfvm_handle* h) {
+  int rc = enqueue_dt(h);
+  if (rc) return rc;
+  if ((rc = run_stage(h, h->U0, h->Ua, 1))) return rc;
+  if ((rc = run_stage(h, h->Ua, h->Ub, 2))) return rc;
+  if ((rc = run_stage(h, h->Ub, h->U0, 3))) return rc;
+  return KFVM_OK;
+}
+
+int enqueue_speed(kfvm_handle* h) {
+  const long long n = (long long)h->g.nx * (h->dim == 3 ? h->g.nm : 1) * h->g.np_loc;
+  CK(cudaMemsetAsync(h->d_smax, 0, sizeof(unsigned long long), h->stream));
+  if (h->dim == 2)
+    k_speed<2><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, h->g, h->d_smax);
+  else
+    k_speed<3><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, h->g, h->d_smax);
+  h->launches++;
+  return KFVM_OK;
+}
+
+int check_err(kfvm_handle* h) {
+  CK(cudaStreamSynchronize(h->stream));
+  int e = 0;
+  CK(cudaMemcpy(&e, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (e) {
+    CK(cudaMemset(h->d_err, 0, sizeof(int)));
+    return fail(h, KFVM_ERR_RUNTIME, "device reported an inadmissible state (NaN, rho<=0 or p<=0)");
+  }
+  return KFVM_OK;
+}
+
+int ensure_dt_cap(kfvm_handle* h, int n) {
+  if (n <= h->dt_cap) return KFVM_OK;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  if (h->d_dt_seq) cudaFree(h->d_dt_seq);
+  h->d_dt_seq = nullptr;
+  CK(cudaMalloc(&h->d_dt_seq, sizeof(double) * n));
+  h->dt_cap = n;
+  return KFVM_OK;
+}
+
+int ensure_aos(kfvm_handle* h) {
+  const size_t n = (size_t)h->g.pstride * h->g.np_loc * h->nv;
+  if (h->aos_elems >= n) return KFVM_OK;
+  if (h->aos) cudaFree(h->aos);
+  CK(cudaMalloc(&h->aos, n * sizeof(double)));
+  h->aos_elems = n;
+  return KFVM_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C-ABI
+extern "C" int kfvm_nccl_unique_id(unsigned char id[128]) {
+  NcclApi& N = nccl();
+  if (!N.ok) return KFVM_ERR_DEVICE;
+  nccl_uid u;
+  if (N.GetUniqueId(&u) != 0) return KFVM_ERR_DEVICE;
+  std::memcpy(id, u.internal, 128);
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, const kfvm_dist* dist,
+                               kfvm_handle** out) {
+  if (!cfg || !t || !out) return KFVM_ERR_CONFIG;
+  *out = nullptr;
+  if ((cfg->dim != 2 && cfg->dim != 3) || (cfg->radius != 2 && cfg->radius != 3) ||
+      t->dim != cfg->dim || t->radius != cfg->radius)
+    return KFVM_ERR_CONFIG;
+  if (cfg->nx < 1 || cfg->ny < 1 || (cfg->dim == 3 && cfg->nz < 1) || !(cfg->dx > 0) ||
+      (cfg->bc != KFVM_BC_PERIODIC && cfg->bc != KFVM_BC_OUTFLOW) ||
+      (cfg->riemann != KFVM_RIEMANN_HLLC && cfg->riemann != KFVM_RIEMANN_HLL))
+    return KFVM_ERR_CONFIG;
+  kfvm_handle* h = new kfvm_handle();
+  h->cfg = *cfg;
+  h->dim = cfg->dim;
+  h->R = cfg->radius;
+  h->nv = cfg->dim + 2;
+  h->NP = t->n_points;
+  if (dist) {
+    h->rank = dist->rank;
+    h->nranks = dist->nranks;
+    h->device = dist->device;
+  }
+  if (cudaSetDevice(h->device) != cudaSuccess) {
+    delete h;
+    return KFVM_ERR_DEVICE;
+  }
+  const int sa = cfg->dim - 1;
+  h->nsa = sa == 2 ? cfg->nz : cfg->ny;
+  if (h->nranks < 1 || h->nranks > h->nsa) {
+    delete h;
+    return KFVM_ERR_CONFIG;
+  }
+  int np;
+  kfvm_slab_range(h->nsa, h->nranks, h->rank, &h->p0, &np);
+  h->g.nx = cfg->nx;
+  h->g.nm = cfg->dim == 3 ? cfg->ny : 1;
+  h->g.np_loc = np;
+  h->g.H = cfg->radius + 1;
+  if (np < h->g.H && h->nranks > 1) {
+    delete h;
+    return fail(nullptr, KFVM_ERR_CONFIG, "slab thinner than the halo");
+  }
+  h->g.pstride = (long long)h->g.nx * h->g.nm;
+  h->g.vstride = h->g.pstride * (np + 2 * h->g.H);
+  // constants (pinned on the host once)
+  DevConsts& k = h->kc;
+  k.dim = cfg->dim;
+  k.nv = h->nv;
+  k.R = cfg->radius;
+  k.riemann = cfg->riemann;
+  k.bc = cfg->bc;
+  k.n[0] = cfg->nx;
+  k.n[1] = h->g.nm;
+  k.n[2] = h->nsa;
+  k.gamma = cfg->gamma;
+  k.gm1 = cfg->gamma - 1.0;
+  k.inv_gm1 = 1.0 / (cfg->gamma - 1.0);
+  k.dx = cfg->dx;
+  k.cfl = cfg->cfl;
+  k.eps = cfg->eps;
+  k.kappa = cfg->kappa;
+  k.kf = cfg->flattener_kf;
+  k.onepk = 1.0 + cfg->kappa;
+  k.onemk = 1.0 - cfg->kappa;
+  k.c13 = 1.0 / 3.0;
+  k.c23 = 2.0 / 3.0;
+  DevTable& T = h->tab;
+  T.n_full = t->n_full;
+  T.n_points = t->n_points;
+  T.n_alpha = t->n_alpha;
+  T.n_stencils = t->n_stencils;
+  T.rp = t->n_points / (2 * t->dim);
+  for (int q = 0; q < t->n_stencils; ++q) {
+    T.size[q] = t->size[q];
+    T.cell_offset[q] = t->cell_offset[q];
+    T.gamma_lin[q] = t->gamma_lin[q];
+  }
+  for (int hh = 0; hh < t->n_full; ++hh) {
+    T.off_x[hh] = t->offsets[3 * hh];
+    if (cfg->dim == 3) {
+      T.off_m[hh] = t->offsets[3 * hh + 1];
+      T.off_p[hh] = t->offsets[3 * hh + 2];
+    } else {
+      T.off_m[hh] = 0;
+      T.off_p[hh] = t->offsets[3 * hh + 1];
+    }
+  }
+  for (int s = 0; s < t->n_points; ++s) T.face_w[s] = t->face_weights[s];
+  for (int a = 0; a < t->n_alpha; ++a) {
+    const int ord = t->alpha[3 * a] + t->alpha[3 * a + 1] + t->alpha[3 * a + 2];
+    double s = 1.0;
+    for (int e = 0; e < 2 * ord; ++e) s *= cfg->dx;  // Delta^(2|alpha|)
+    T.scale[a] = s;
+  }
+  int rc = KFVM_OK;
+  auto bad = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rc == KFVM_OK) {
+      rc = KFVM_ERR_DEVICE;
+      h->err = std::string(what) + ": " + cudaGetErrorString(e);
+    }
+  };
+  const size_t nface = (size_t)t->total_cells * t->n_points;
+  const size_t nder = (size_t)t->total_cells * t->n_alpha;
+  bad(cudaMalloc(&h->d_face, nface * sizeof(double)), "cudaMalloc face");
+  bad(cudaMalloc(&h->d_deriv, nder * sizeof(double)), "cudaMalloc deriv");
+  if (rc == KFVM_OK) {
+    bad(cudaMemcpy(h->d_face, t->face, nface * sizeof(double), cudaMemcpyHostToDevice), "copy face");
+    bad(cudaMemcpy(h->d_deriv, t->deriv, nder * sizeof(double), cudaMemcpyHostToDevice), "copy deriv");
+  }
+  T.face = h->d_face;
+  T.deriv = h->d_deriv;
+  T.gather = nullptr;
+  bad(cudaMemcpyToSymbol(c_k, &k, sizeof(k)), "constants");
+  bad(cudaMemcpyToSymbol(c_t, &T, sizeof(T)), "table");
+  bad(cudaMemcpyToSymbol(c_gather, t->gather, sizeof(int) * t->total_cells), "gather");
+  const size_t ufull = (size_t)h->g.vstride * h->nv;
+  bad(cudaMalloc(&h->U0, ufull * sizeof(double)), "cudaMalloc U0");
+  bad(cudaMalloc(&h->Ua, ufull * sizeof(double)), "cudaMalloc Ua");
+  bad(cudaMalloc(&h->Ub, ufull * sizeof(double)), "cudaMalloc Ub");
+  if (rc == KFVM_OK) {
+    bad(cudaMemset(h->U0, 0, ufull * sizeof(double)), "memset");
+    bad(cudaMemset(h->Ua, 0, ufull * sizeof(double)), "memset");
+    bad(cudaMemset(h->Ub, 0, ufull * sizeof(double)), "memset");
+  }
+  // chunk planes so the face-state scratch stays within budget
+  {
+    const long long per_plane = (long long)(h->g.nx + 2) * (h->dim == 3 ? h->g.nm + 2 : 1) *
+                                h->NP * h->nv * (long long)sizeof(double);
+    long long c = h->st_budget / per_plane - 2;
+    c = std::max(1LL, std::min(c, (long long)np));
+    h->chunk = (int)c;
+  }
+  {
+    const Chunk ch = make_chunk(h, 0, h->chunk);
+    h->st_elems = (size_t)ch.next * h->NP * h->nv;
+    h->f_elems = (size_t)ch.nfb * h->dim * h->nv;
+    bad(cudaMalloc(&h->St, h->st_elems * sizeof(double)), "cudaMalloc states");
+    bad(cudaMalloc(&h->F, h->f_elems * sizeof(double)), "cudaMalloc flux");
+  }
+  bad(cudaMalloc(&h->d_dt_cur, sizeof(double)), "cudaMalloc dt");
+  bad(cudaMalloc(&h->d_smax, sizeof(unsigned long long)), "cudaMalloc smax");
+  bad(cudaMalloc(&h->d_step, sizeof(int)), "cudaMalloc step");
+  bad(cudaMalloc(&h->d_err, sizeof(int)), "cudaMalloc err");
+  if (rc == KFVM_OK) {
+    bad(cudaMemset(h->d_err, 0, sizeof(int)), "memset");
+    bad(cudaMemset(h->d_step, 0, sizeof(int)), "memset");
+    bad(cudaMemset(h->d_smax, 0, sizeof(unsigned long long)), "memset");
+  }
+  bad(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
+  bad(cudaEventCreate(&h->ev[0]), "event");
+  bad(cudaEventCreate(&h->ev[1]), "event");
+  if (rc == KFVM_OK) rc = ensure_dt_cap(h, 1024);
+  if (rc == KFVM_OK && h->nranks > 1) {
+    NcclApi& N = nccl();
+    if (!N.ok) {
+      rc = KFVM_ERR_DEVICE;
+      h->err = "libnccl.so.2 not loadable";
+    } else {
+      nccl_uid u;
+      std::memcpy(u.internal, dist->nccl_id, 128);
+      if (N.CommInitRank(&h->comm, h->nranks, u, h->rank) != 0) {
+        rc = KFVM_ERR_DEVICE;
+        h->err = "ncclCommInitRank failed";
+      }
+    }
+  }
+  if (rc != KFVM_OK) {
+    fprintf(stderr, "kfvm_gpu_create: %s\n", h->err.c_str());
+    kfvm_gpu_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return KFVM_OK;
+}
+
+extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
+  if (!h) return;
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->comm) nccl().CommDestroy(h->comm);
+  for (void* p : {(void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->St, (void*)h->F,
+                  (void*)h->aos, (void*)h->d_face, (void*)h->d_deriv, (void*)h->d_dt_seq,
+                  (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err})
+    if (p) cudaFree(p);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+extern "C" int kfvm_gpu_set_state_device(kfvm_handle* h, const double* U_dev) {
+  const long long n = h->g.pstride * h->g.np_loc * h->nv;
+  k_transpose<0><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, const_cast<double*>(U_dev), h->g,
+                                                         h->nv);
+  h->launches++;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_get_state_device(kfvm_handle* h, double* U_dev) {
+  const long long n = h->g.pstride * h->g.np_loc * h->nv;
+  k_transpose<1><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, U_dev, h->g, h->nv);
+  h->launches++;
+  CK(cudaStreamSynchronize(h->stream));
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_set_state(kfvm_handle* h, const double* U_host) {
+  int rc = ensure_aos(h);
+  if (rc) return rc;
+  const size_t n = (size_t)h->g.pstride * h->g.np_loc * h->nv;
+  CK(cudaMemcpyAsync(h->aos, U_host, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  return kfvm_gpu_set_state_device(h, h->aos);
+}
+
+extern "C" int kfvm_gpu_get_state(kfvm_handle* h, double* U_host) {
+  int rc = ensure_aos(h);
+  if (rc) return rc;
+  rc = kfvm_gpu_get_state_device(h, h->aos);
+  if (rc) return rc;
+  const size_t n = (size_t)h->g.pstride * h->g.np_loc * h->nv;
+  CK(cudaMemcpyAsync(U_host, h->aos, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_rhs(kfvm_handle* h, double* dUdt_host) {
+  int rc = run_stage(h, h->U0, h->Ua, 0);
+  if (rc) return rc;
+  if ((rc = check_err(h))) return rc;
+  if ((rc = ensure_aos(h))) return rc;
+  const long long n = h->g.pstride * h->g.np_loc * h->nv;
+  k_transpose<1><<<blocks(n, 256), 256, 0, h->stream>>>(h->Ua, h->aos, h->g, h->nv);
+  h->launches++;
+  CK(cudaMemcpyAsync(dUdt_host, h->aos, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_states(kfvm_handle* h, double* states_host) {
+  int rc = halo(h, h->U0);
+  if (rc) return rc;
+  const long long per_cell = (long long)h->NP * h->nv;
+  const long long plane_cells = h->g.pstride;
+  double* dbuf = nullptr;
+  CK(cudaMalloc(&dbuf, (size_t)plane_cells * h->chunk * per_cell * sizeof(double)));
+  for (int c0 = 0; c0 < h->g.np_loc; c0 += h->chunk) {
+    const Chunk ch = make_chunk(h, c0, std::min(h->chunk, h->g.np_loc - c0));
+    states_and_flux(h, h->U0, ch);
+    const long long n = plane_cells * ch.C * per_cell;
+    if (h->dim == 2)
+      k_extract_states<2><<<blocks(n, 256), 256, 0, h->stream>>>(h->St, dbuf, h->g, ch, h->NP);
+    else
+      k_extract_states<3><<<blocks(n, 256), 256, 0, h->stream>>>(h->St, dbuf, h->g, ch, h->NP);
+    h->launches++;
+    cudaMemcpyAsync(states_host + plane_cells * c0 * per_cell, dbuf, n * sizeof(double),
+                    cudaMemcpyDeviceToHost, h->stream);
+  }
+  cudaStreamSynchronize(h->stream);
+  cudaFree(dbuf);
+  return check_err(h);
+}
+
+extern "C" int kfvm_gpu_select_dt(kfvm_handle* h, double* dt) {
+  int rc = enqueue_speed(h);
+  if (rc) return rc;
+  if ((rc = reduce_smax(h))) return rc;
+  unsigned long long bits = 0;
+  CK(cudaMemcpyAsync(&bits, h->d_smax, sizeof(bits), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  double s;
+  std::memcpy(&s, &bits, sizeof(s));
+  *dt = (h->cfg.cfl * h->cfg.dx) / s;
+  return (*dt > 0 && std::isfinite(*dt)) ? KFVM_OK : fail(h, KFVM_ERR_RUNTIME, "bad dt");
+}
+
+extern "C" int kfvm_gpu_stage(kfvm_handle* h, int stage, double dt) {
+  if (stage < 1 || stage > 3) return fail(h, KFVM_ERR_CONFIG, "stage must be 1..3");
+  CK(cudaMemcpyAsync(h->d_dt_cur, &dt, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  double* in = stage == 1 ? h->U0 : (stage == 2 ? h->Ua : h->Ub);
+  double* outp = stage == 1 ? h->Ua : (stage == 2 ? h->Ub : h->U0);
+  int rc = run_stage(h, in, outp, stage);
+  if (rc) return rc;
+  return check_err(h);
+}
+
+extern "C" int kfvm_gpu_run_async(kfvm_handle* h, int nsteps) {
+  int rc = ensure_dt_cap(h, nsteps);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
+  if ((rc = enqueue_speed(h))) return rc;
+  if (h->timing || h->nranks > 1) {
+    for (int s = 0; s < nsteps; ++s)
+      if ((rc = enqueue_step(h))) return rc;
+    return KFVM_OK;
+  }
+  if (!h->graph) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    const long long l0 = h->launches;
+    rc = enqueue_step(h);
+    cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(h, KFVM_ERR_DEVICE, "graph capture failed");
+    CK(cudaGraphInstantiate(&h->graph, graph, 0));
+    cudaGraphDestroy(graph);
+    h->launches = l0;
+  }
+  long long per_step = 0;
+  {
+    const int nchunks = (h->g.np_loc + h->chunk - 1) / h->chunk;
+    per_step = 1 + 3 * (1 + 3LL * nchunks);
+  }
+  for (int s = 0; s < nsteps; ++s) CK(cudaGraphLaunch(h->graph, h->stream));
+  h->launches += per_step * nsteps;
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_sync(kfvm_handle* h) { return check_err(h); }
+
+extern "C" int kfvm_gpu_dt_sequence(kfvm_handle* h, double* dt_seq, int nsteps) {
+  if (nsteps > h->dt_cap) return fail(h, KFVM_ERR_CONFIG, "nsteps exceeds dt capacity");
+  CK(cudaMemcpyAsync(dt_seq, h->d_dt_seq, sizeof(double) * nsteps, cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_run(kfvm_handle* h, int nsteps, double* dt_seq) {
+  int rc = kfvm_gpu_run_async(h, nsteps);
+  if (rc) return rc;
+  if ((rc = kfvm_gpu_sync(h))) return rc;
+  if (dt_seq) return kfvm_gpu_dt_sequence(h, dt_seq, nsteps);
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_step(kfvm_handle* h, double* dt_out) {
+  double dt;
+  int rc = kfvm_gpu_run(h, 1, &dt);
+  if (rc) return rc;
+  if (dt_out) *dt_out = dt;
+  return KFVM_OK;
+}
+
+extern "C" void* kfvm_gpu_stream(kfvm_handle* h) { return (void*)h->stream; }
+extern "C" long long kfvm_gpu_launch_count(kfvm_handle* h) { return h->launches; }
+
+extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long value) {
+  std::string n(name ? name : "");
+  if (n == "timing") {
+    h->timing = value != 0;
+    h->t_states = h->t_flux = h->t_update = h->t_other = 0;
+    return KFVM_OK;
+  }
+  if (n == "chunk_planes" || n == "scratch_bytes") {
+    long long c;
+    if (n == "chunk_planes") {
+      c = value;
+    } else {
+      const long long per_plane = (long long)(h->g.nx + 2) * (h->dim == 3 ? h->g.nm + 2 : 1) *
+                                  h->NP * h->nv * (long long)sizeof(double);
+      c = value / per_plane - 2;
+    }
+    c = std::max(1LL, std::min(c, (long long)h->g.np_loc));
+    if (h->graph) {
+      cudaGraphExecDestroy(h->graph);
+      h->graph = nullptr;
+    }
+    cudaFree(h->St);
+    cudaFree(h->F);
+    h->St = h->F = nullptr;
+    h->chunk = (int)c;
+    const Chunk ch = make_chunk(h, 0, h->chunk);
+    h->st_elems = (size_t)ch.next * h->NP * h->nv;
+    h->f_elems = (size_t)ch.nfb * h->dim * h->nv;
+    CK(cudaMalloc(&h->St, h->st_elems * sizeof(double)));
+    CK(cudaMalloc(&h->F, h->f_elems * sizeof(double)));
+    return KFVM_OK;
+  }
+  return fail(h, KFVM_ERR_CONFIG, "unknown option " + n);
+}
+
+extern "C" int kfvm_gpu_kernel_times(kfvm_handle* h, double* a, double* b, double* c, double* d) {
+  if (a) *a = h->t_states;
+  if (b) *b = h->t_flux;
+  if (c) *c = h->t_update;
+  if (d) *d = h->t_other;
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_last_error(kfvm_handle* h, char* buf, size_t n) {
+  if (!buf || n == 0) return KFVM_ERR_CONFIG;
+  const std::string& e = h ? h->err : std::string("null handle");
+  std::snprintf(buf, n, "%s", e.c_str());
+  return KFVM_OK;
+}
+
+// Seeded IC generated on the device directly into the handle's state (used
+// by the bench at sizes where the host generator is slow); bit-identical to
+// kfvm_ic_generate (same arithmetic, tables from the host).
+extern "C" int kfvm_gpu_ic_generate(kfvm_handle* h, const kfvm_ic_params* ic) {
+  if (ic->kind != KFVM_IC_FOURIER && ic->kind != KFVM_IC_VORONOI &&
+      ic->kind != KFVM_IC_FOURIER_SPHERE && ic->kind != KFVM_IC_UNIFORM)
+    return fail(h, KFVM_ERR_CONFIG, "IC kind not available on the device");
+  ICHostPlan hp;
+  int rc = ic_plan_build(&h->cfg, ic, &hp);
+  if (rc) return fail(h, rc, "bad IC parameters");
+  ICPlan P = hp.plan;
+  std::vector<void*> tmp;
+  for (int a = 0; a < P.dim; ++a) {
+    if (hp.fc[a].empty()) continue;
+    double *dc, *ds;
+    CK(cudaMalloc(&dc, hp.fc[a].size() * sizeof(double)));
+    CK(cudaMalloc(&ds, hp.fs[a].size() * sizeof(double)));
+    CK(cudaMemcpy(dc, hp.fc[a].data(), hp.fc[a].size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ds, hp.fs[a].data(), hp.fs[a].size() * sizeof(double), cudaMemcpyHostToDevice));
+    P.fc[a] = dc;
+    P.fs[a] = ds;
+    tmp.push_back(dc);
+    tmp.push_back(ds);
+  }
+  ICPlan* dP;
+  CK(cudaMalloc(&dP, sizeof(ICPlan)));
+  tmp.push_back(dP);
+  CK(cudaMemcpy(dP, &P, sizeof(ICPlan), cudaMemcpyHostToDevice));
+  if (hp.needs_norm) {
+    unsigned long long* dm;
+    CK(cudaMalloc(&dm, sizeof(unsigned long long)));
+    tmp.push_back(dm);
+    const long long n = (long long)h->g.nx * h->g.nm * h->nsa;
+    for (int f = 0; f < 1 + P.dim; ++f) {
+      CK(cudaMemset(dm, 0, sizeof(unsigned long long)));
+      k_ic_norm<<<blocks(n, 128), 128>>>(dP, f, h->g, h->p0, dm);
+      unsigned long long bits;
+      CK(cudaMemcpy(&bits, dm, sizeof(bits), cudaMemcpyDeviceToHost));
+      std::memcpy(&P.f[f].norm, &bits, sizeof(double));
+    }
+    CK(cudaMemcpy(dP, &P, sizeof(ICPlan), cudaMemcpyHostToDevice));
+  }
+  const long long n = (long long)h->g.nx * h->g.nm * h->g.np_loc;
+  k_ic_fill<<<blocks(n, 128), 128>>>(dP, h->U0, h->g, h->p0);
+  CK(cudaDeviceSynchronize());
+  for (void* p : tmp) cudaFree(p);
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  CK(cudaMemset(h->d_step, 0, sizeof(int)));
+  return KFVM_OK;
+}
+
+// ------------------------------------------------------- FP64 peak probes
+// DFMA: 8 independent FMA chains per thread; DMMA: mma.sync m8n8k4 f64.
+// Used once per pool to measure the roofline denominator.
+namespace kfvm_b200 {
+__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void k_dmma_peak(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+            : "+d"(c[i][0]), "+d"(c[i][1])
+            : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;
+}
+}  // namespace kfvm_b200
+
+extern "C" int kfvm_fp64_peak(double* dfma_tflops, double* dmma_tflops, double* sm_clock_ghz) {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  double* d;
+  if (cudaMalloc(&d, 64) != cudaSuccess) return KFVM_ERR_DEVICE;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int threads = 512, iters = 4096;
+  const int grid = nsm * 4;
+  float ms = 0;
+  k_dfma_peak<<<grid, threads>>>(d, 16, 0.999, 1e-3);
+  cudaEventRecord(e0);
+  k_dfma_peak<<<grid, threads>>>(d, iters, 0.999, 1e-3);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double dfma = 2.0 * 8 * 16 * (double)iters * threads * grid;
+  if (dfma_tflops) *dfma_tflops = dfma / (ms * 1e-3) / 1e12;
+  k_dmma_peak<<<grid, threads>>>(d, 16);
+  cudaEventRecord(e0);
+  k_dmma_peak<<<grid, threads>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  // one m8n8k4 per warp = 8*8*4 FMA = 512 flops
+  const double dmma = 512.0 * 4 * 16 * (double)iters * (threads / 32) * grid;
+  if (dmma_tflops) *dmma_tflops = dmma / (ms * 1e-3) / 1e12;
+  if (sm_clock_ghz) {
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
+    *sm_clock_ghz = khz * 1e-6;
+  }
+  cudaFree(d);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return cudaGetLastError() == cudaSuccess ? KFVM_OK : KFVM_ERR_DEVICE;
+}

@@ -1,0 +1,128 @@
+"""GPU parity against the CPU oracle through the C-ABI (BASELINE.json
+north_star gate: relative L1 <= 1e-11 per conserved variable after the stated
+steps, identical dt sequence).  The implementation targets bit-identity
+(pinned FP contract); the max ulp difference is asserted == 0
+where the contract guarantees it."""
+import numpy as np
+import pytest
+
+import paper_2401_16543_b200 as K
+from paper_2401_16543_b200.config import ICSpec
+from oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11  # relative L1 per conserved variable (north_star)
+
+
+def rel_l1(a, b):
+    ax = tuple(range(a.ndim - 1))
+    return np.abs(a - b).sum(axis=ax) / np.maximum(np.abs(b).sum(axis=ax), 1e-300)
+
+
+def max_ulp(a, b):
+    d = np.abs(a.view(np.int64) - b.view(np.int64))
+    return int(d.max()) if a.size else 0
+
+
+CASES = [
+    # (name, config index, n, steps, overrides)
+    ("cfg1_2d_r2_periodic_fourier", 1, 32, 3, {}),
+    ("cfg2_2d_r2_outflow_voronoi", 2, 40, 3, {}),
+    ("cfg1_2d_r3_periodic_hll", 1, 24, 2, {"radius": 3, "riemann": "hll"}),
+    ("cfg3_3d_r2_periodic_fourier", 3, 16, 2, {}),
+    ("cfg4_3d_r2_outflow_voronoi", 4, 14, 2, {}),
+    ("cfg5_3d_r3_periodic_sphere", 5, 12, 1, {}),
+]
+
+
+def _setup(idx, n, over):
+    from dataclasses import replace
+    w = K.baseline_config(idx, n=n)
+    g = replace(w.grid, **over) if over else w.grid
+    U = K.initial_condition(g, w.ic)
+    rset = K.precompute(g.radius, dim=g.dim)
+    return g, w.ic, U, rset
+
+
+@pytest.mark.parametrize("name,idx,n,steps,over", CASES, ids=[c[0] for c in CASES])
+def test_run_parity(require_gpu, name, idx, n, steps, over):
+    g, ic, U, rset = _setup(idx, n, over)
+    with K.Solver(g, rset) as s:
+        s.set_state(U)
+        dts = s.advance(steps)
+        Ug = s.get_state()
+    Uo, dto = Oracle(g, rset).run(U, steps)
+    assert np.array_equal(dts, dto), (dts, dto)
+    err = rel_l1(Ug, Uo)
+    assert (err <= TOL).all(), err
+    assert np.array_equal(Ug, Uo), f"max ulp {max_ulp(Ug, Uo)}"
+
+
+@pytest.mark.parametrize("idx,n", [(1, 24), (3, 10), (4, 10)])
+def test_rhs_and_states_parity(require_gpu, idx, n):
+    g, ic, U, rset = _setup(idx, n, {})
+    o = Oracle(g, rset)
+    with K.Solver(g, rset) as s:
+        Lg = s.compute_rhs(U)
+        Sg = s.reconstruct_states(U)
+        dtg = s.select_dt(U)
+    assert np.array_equal(Lg, o.compute_rhs(U))
+    assert np.array_equal(Sg, o.reconstruct_states(U))
+    assert dtg == o.select_dt(U)
+
+
+def test_stage_api_matches_run(require_gpu):
+    g, ic, U, rset = _setup(1, 20, {})
+    with K.Solver(g, rset) as s:
+        s.set_state(U)
+        dt = s.select_dt()
+        for st in (1, 2, 3):
+            s.ssp_rk3_stage(st, dt)
+        U1 = s.get_state()
+    Uo, dto = Oracle(g, rset).run(U, 1)
+    assert dt == dto[0]
+    assert np.array_equal(U1, Uo)
+
+
+def test_chunked_equals_unchunked(require_gpu):
+    g, ic, U, rset = _setup(3, 12, {})
+    with K.Solver(g, rset) as s:
+        s.set_state(U)
+        d1 = s.advance(2)
+        A = s.get_state()
+    with K.Solver(g, rset) as s:
+        s.set_option("chunk_planes", 5)
+        s.set_state(U)
+        d2 = s.advance(2)
+        B = s.get_state()
+    assert np.array_equal(d1, d2) and np.array_equal(A, B)
+
+
+def test_device_ic_matches_host(require_gpu):
+    for idx, n in ((1, 32), (2, 32), (3, 12), (4, 12), (5, 10)):
+        w = K.baseline_config(idx, n=n)
+        U = K.initial_condition(w.grid, w.ic)
+        with K.Solver(w.grid) as s:
+            s.generate_ic(w.ic)
+            Ud = s.get_state()
+        assert np.array_equal(U, Ud), idx
+
+
+def test_free_stream_preserved(require_gpu):
+    g = K.GridConfig(dim=3, radius=2, nx=12, ny=12, nz=12, cfl=0.3)
+    U = K.initial_condition(g, ICSpec("uniform", value=(1.3, 0.7, -0.4, 0.2, 2.0)))
+    with K.Solver(g) as s:
+        s.set_state(U)
+        s.advance(3)
+        assert np.array_equal(s.get_state(), U)
+
+
+def test_runtime_error_on_inadmissible_state(require_gpu):
+    g = K.GridConfig(dim=2, radius=2, nx=16, ny=16, cfl=0.4)
+    U = K.initial_condition(g, ICSpec("uniform", value=(1.0, 0.0, 0.0, 0.0, 1.0)))
+    U[5, 5, 0] = -1.0
+    with K.Solver(g) as s:
+        s.set_state(U)
+        with pytest.raises(K.KfvmRuntimeError):
+            s.advance(1)
