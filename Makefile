@@ -8,7 +8,8 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 CXX ?= g++
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CXXFLAGS := -std=gnu++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra
-NVFLAGS := $(ARCH) -std=c++17 -O3 -lineinfo -fmad=false -Xcompiler -fPIC,-ffp-contract=off \
+MINB ?= 2
+NVFLAGS := $(ARCH) -DKFVM_FAST_MINB=$(MINB) -std=c++17 -O3 -lineinfo -fmad=false -Xcompiler -fPIC,-ffp-contract=off \
            -Xptxas -v --expt-relaxed-constexpr
 
 PKG := paper_2401_16543_b200
@@ -28,7 +29,10 @@ $(BUILD)/kfvm_table.o: $(SRC)/kfvm_table.cpp include/kfvm_b200.h | $(BUILD)
 $(BUILD)/kfvm_ic.o: $(SRC)/kfvm_ic.cpp $(SRC)/kfvm_ic_eval.h $(SRC)/kfvm_ic_host.h include/kfvm_b200.h | $(BUILD)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(BUILD)/kfvm_gpu.o: $(SRC)/kfvm_gpu.cu $(SRC)/kfvm_device.cuh $(SRC)/kfvm_ic_eval.h include/kfvm_b200.h | $(BUILD)
+$(SRC)/kfvm_gen.cuh: tools/gen_kernels.py
+	python tools/gen_kernels.py
+
+$(BUILD)/kfvm_gpu.o: $(SRC)/kfvm_gpu.cu $(SRC)/kfvm_gen.cuh $(SRC)/kfvm_device.cuh $(SRC)/kfvm_ic_eval.h include/kfvm_b200.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_kfvm_gpu.txt || (cat $(BUILD)/ptxas_kfvm_gpu.txt; false)
 
 $(LIB): $(BUILD)/kfvm_table.o $(BUILD)/kfvm_ic.o $(BUILD)/kfvm_gpu.o

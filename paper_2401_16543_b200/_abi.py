@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkfvm_b200.so")
+LIB_PATH = os.environ.get("KFVM_LIB") or os.path.join(_HERE, "libkfvm_b200.so")
 
 KFVM_OK, KFVM_ERR_CONFIG, KFVM_ERR_RUNTIME, KFVM_ERR_DEVICE = 0, 1, 2, 3
 BC_PERIODIC, BC_OUTFLOW = 0, 1

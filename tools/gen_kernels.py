@@ -1,0 +1,203 @@
+#!/usr/bin/env python
+"""Generate paper_2401_16543_b200/csrc/kfvm_gen.cuh — fully unrolled sparse
+stencil contractions of the KFVM-WENO reconstruction for (dim, R) in
+{(2,2), (2,3), (3,2)}.
+
+The generated code is the device form of the oracle's weno_field
+(oracle/kfvm_oracle.cpp): for every (sub)stencil q it evaluates the n_alpha
+derivative dot products (beta_q), the nonlinear weights
+and, for every face point s, the WENO-AO combination of the per-stencil point
+values, each dot product accumulated in stencil order from 0.0 with
+explicit fma — the pinned FP contract.  Because the gather pattern is known at
+compile time, the stencil values live in registers and every weight is a
+__constant__ operand with a literal offset (DFMA R, R, c[bank][imm], R): the
+inner loop issues nothing but DFMAs.
+
+Only the sparsity structure is generated (it follows from the stencil
+geometry, proj/core/src/geometry.cpp:10-34 and PAPER.md §3.1); the weight
+values are uploaded at run time from the binary128 table, and
+kfvm_gpu_create checks the table's gather/offset arrays against the
+structure compiled in here.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "paper_2401_16543_b200", "csrc", "kfvm_gen.cuh")
+
+CASES = [(2, 2), (2, 3), (3, 2)]
+
+
+def full_stencil(dim, R):
+    kr = R if dim == 3 else 0
+    out = []
+    for k in range(-kr, kr + 1):
+        for j in range(-R, R + 1):
+            for i in range(-R, R + 1):
+                if i * i + j * j + k * k <= R * R:
+                    out.append((i, j, k))
+    return out
+
+
+def in_sub(dim, R, q, o):
+    if q == 1:
+        return sum(c * c for c in o) <= (R - 1) ** 2
+    axis = (q - 2) // 2
+    sgn = -1 if (q - 2) % 2 else 1
+    a = sgn * o[axis]
+    return all(abs(o[t]) <= a for t in range(dim) if t != axis)
+
+
+def graded(dim, lo, hi):
+    out = []
+    for n in range(lo, hi + 1):
+        if dim == 2:
+            out += [(n - k, k, 0) for k in range(n + 1)]
+        else:
+            for a in range(n, -1, -1):
+                for b in range(n - a, -1, -1):
+                    out.append((a, b, n - a - b))
+    return out
+
+
+def gen_case(dim, R):
+    full = full_stencil(dim, R)
+    ns = 2 * dim + 2
+    members = [list(range(len(full)))]
+    for q in range(1, ns):
+        members.append([h for h, o in enumerate(full) if in_sub(dim, R, q, o)])
+    sizes = [len(m) for m in members]
+    offs, acc = [], 0
+    for n in sizes:
+        offs.append(acc)
+        acc += n
+    total = acc
+    na = len(graded(dim, 1, R))
+    npnt = 2 * dim * R ** (dim - 1)
+    tag = f"{dim}{R}"
+    L = []
+    L.append(f"// ---- dim={dim} R={R}: N0={len(full)} sizes={sizes} n_alpha={na} n_points={npnt}")
+    L.append(f"__constant__ __align__(16) double c_f{tag}[{total * npnt}];  // table.face transposed, [q][h][s]")
+    L.append(f"__constant__ __align__(16) double c_d{tag}[{total * (na + (na & 1))}];  // table.deriv, [q][h][a] padded")
+    L.append(f"template <> struct Gen<{dim}, {R}> {{")
+    L.append(f"  static constexpr int N0 = {len(full)}, NP = {npnt}, NA = {na}, NS = {ns}, NTOT = {total};")
+    L.append(f"  static constexpr int OFF[{len(full)}][3] = {{" +
+             ", ".join("{%d, %d, %d}" % o for o in full) + "};")
+    L.append("  __host__ __device__ static constexpr int off(int h, int a) {")
+    L.append(f"    constexpr int T[{len(full)}][3] = {{" + ", ".join("{%d, %d, %d}" % o for o in full) + "};")
+    L.append("    return T[h][a];")
+    L.append("  }")
+    flat = [h for m in members for h in m]
+    L.append(f"  static constexpr int GATHER[{total}] = {{" + ", ".join(map(str, flat)) + "};")
+    # sizes as constexpr functions (usable in device code after unrolling)
+    L.append("  __host__ __device__ static constexpr int qsize(int q) {")
+    L.append("    return " + " : ".join(f"q == {q} ? {sizes[q]}" for q in range(ns - 1)) + f" : {sizes[-1]};")
+    L.append("  }")
+    L.append("  __host__ __device__ static constexpr int kc(int q) { return (qsize(q) + 3) / 4; }")
+    L.append("  __host__ __device__ static constexpr int cbase(int q) { return q == 0 ? 0 : cbase(q - 1) + kc(q - 1); }")
+    L.append(f"  static constexpr int NCHUNK = {sum((n + 3) // 4 for n in sizes)};")
+    L.append("  static const void* face_symbol() { return (const void*)&c_f%s; }" % tag)
+    L.append("  static const void* deriv_symbol() { return (const void*)&c_d%s; }" % tag)
+    # WENO body, outer-product form: for each stencil q loop over its cells h
+    # (runtime loop) and update NA (derivatives) or NP (face points)
+    # independent accumulators per step -> ILP NA / NP, tiny code.  Weights are
+    # stored transposed, [q][h][a] and [q][h][s], so one h row is contiguous
+    # (LDCU.128).  Every dot product still accumulates over h in stencil
+    # order from 0.0 (the pinned FP contract).
+    nap = na + (na & 1)
+    L.append(f"  static constexpr int NAP = {nap};  // padded derivative row")
+    L.append("  // g of this thread lives in shared memory: g[h] = sg[h * gstride]")
+    L.append("  static __device__ __forceinline__ void weno(const double* sg, int gstride, double* sw,")
+    L.append("                                              int sstride, const double* __restrict__ sc,")
+    L.append("                                              const double* __restrict__ gam, double eps,")
+    L.append("                                              const int* __restrict__ gat) {")
+    for q in range(ns):
+        L.append(f"    double b{q};")
+    for q in range(ns):
+        N, o = sizes[q], offs[q]
+        L.append("    {")
+        L.append(f"      double d[{nap}];")
+        L.append("#pragma unroll")
+        L.append(f"      for (int a = 0; a < {nap}; ++a) d[a] = 0.0;")
+        L.append("#pragma unroll 1")
+        L.append(f"      for (int h = 0; h < {N}; ++h) {{")
+        L.append(f"        const double gh = sg[gat[{o} + h] * gstride];")
+        L.append(f"        const double2* W = reinterpret_cast<const double2*>(c_d{tag} + ({o} + h) * {nap});")
+        L.append("#pragma unroll")
+        L.append(f"        for (int a = 0; a < {nap // 2}; ++a) {{")
+        L.append("          const double2 w2 = W[a];")
+        L.append("          d[2 * a] = fma(w2.x, gh, d[2 * a]);")
+        if na % 2:
+            L.append(f"          if (2 * a + 1 < {na}) d[2 * a + 1] = fma(w2.y, gh, d[2 * a + 1]);")
+        else:
+            L.append("          d[2 * a + 1] = fma(w2.y, gh, d[2 * a + 1]);")
+        L.append("        }")
+        L.append("      }")
+        L.append(f"      b{q} = 0.0;")
+        L.append("#pragma unroll")
+        L.append(f"      for (int a = 0; a < {na}; ++a) b{q} = fma(sc[a], d[a] * d[a], b{q});")
+        L.append("    }")
+    L.append(f"    double om[{ns}];")
+    for q in range(ns):
+        L.append(f"    om[{q}] = gam[{q}] / fma(b{q}, b{q}, eps);")
+    L.append("    double sum = om[0];")
+    L.append("#pragma unroll")
+    L.append(f"    for (int q = 1; q < {ns}; ++q) sum = sum + om[q];")
+    L.append("#pragma unroll")
+    L.append(f"    for (int q = 0; q < {ns}; ++q) om[q] = om[q] / sum;")
+    L.append("    const double c0 = om[0] / gam[0];")
+    L.append(f"    double v[{npnt}];")
+    for q in range(ns):
+        N, o = sizes[q], offs[q]
+        L.append("    {")
+        L.append(f"      const double c = {'c0' if q == 0 else f'fma(-c0, gam[{q}], om[{q}])'};")
+        L.append(f"      double p[{npnt}];")
+        L.append("#pragma unroll")
+        L.append(f"      for (int s = 0; s < {npnt}; ++s) p[s] = 0.0;")
+        L.append("#pragma unroll 1")
+        L.append(f"      for (int h = 0; h < {N}; ++h) {{")
+        L.append(f"        const double gh = sg[gat[{o} + h] * gstride];")
+        L.append(f"        const double2* W = reinterpret_cast<const double2*>(c_f{tag} + ({o} + h) * {npnt});")
+        L.append("#pragma unroll")
+        L.append(f"        for (int s = 0; s < {npnt // 2}; ++s) {{")
+        L.append("          const double2 w2 = W[s];")
+        L.append("          p[2 * s] = fma(w2.x, gh, p[2 * s]);")
+        L.append("          p[2 * s + 1] = fma(w2.y, gh, p[2 * s + 1]);")
+        L.append("        }")
+        L.append("      }")
+        L.append("#pragma unroll")
+        if q == 0:
+            L.append(f"      for (int s = 0; s < {npnt}; ++s) v[s] = c * p[s];")
+        else:
+            L.append(f"      for (int s = 0; s < {npnt}; ++s) v[s] = fma(c, p[s], v[s]);")
+        L.append("    }")
+    L.append("#pragma unroll")
+    L.append(f"    for (int s = 0; s < {npnt}; ++s) sw[s * sstride] = v[s];")
+    L.append("  }")
+    L.append("};")
+    return "\n".join(L)
+
+
+def main():
+    parts = [
+        "// AUTO-GENERATED by tools/gen_kernels.py — do not edit by hand.",
+        "// Unrolled sparse stencil contractions (see the generator's docstring).",
+        "#ifndef KFVM_GEN_CUH_",
+        "#define KFVM_GEN_CUH_",
+        "namespace kfvm_b200 {",
+        "template <int D, int R> struct Gen;",
+    ]
+    for d, r in CASES:
+        parts.append(gen_case(d, r))
+    parts += ["}  // namespace kfvm_b200", "#endif", ""]
+    src = "\n".join(parts)
+    if os.path.exists(OUT) and open(OUT).read() == src:
+        return
+    with open(OUT, "w") as f:
+        f.write(src)
+
+
+if __name__ == "__main__":
+    main()
