@@ -203,6 +203,8 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override resolution (testing)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--engine", type=int, default=None,
+                    help="reconstruction kernel: 0 generic, 1 DFMA, 2 DMMA (default: per dim)")
     args = ap.parse_args()
 
     import paper_2401_16543_b200 as K
@@ -231,6 +233,8 @@ def main():
     g = w.grid
     s = K.Solver(g, rset, rank=rank, nranks=ws, device=local, nccl_id=nccl_id)
     stream = torch.cuda.ExternalStream(s.stream)
+    if args.engine is not None:
+        s.set_option("engine", args.engine)
 
     # warm-up (also captures the CUDA graph)
     s.generate_ic(w.ic)

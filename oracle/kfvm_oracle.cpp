@@ -76,6 +76,15 @@ inline double pressure(int dim, const double* U, double gm1) {
   return gm1 * (U[dim + 1] - 0.5 * (q / U[0]));
 }
 
+// p(U) < pmin for a state with rho > 0, written without the division:
+// gm1 (E rho - |m|^2 / 2) < pmin rho  (used by the limiter)
+inline bool p_below(int dim, const double* U, double gm1, double pmin) {
+  double q = U[1] * U[1];
+  q = fma(U[2], U[2], q);
+  if (dim == 3) q = fma(U[3], U[3], q);
+  return gm1 * fma(U[dim + 1], U[0], -0.5 * q) < pmin * U[0];
+}
+
 inline double sound(double gamma, double p, double rho) {
   return std::sqrt((gamma * p) / rho);
 }
@@ -137,15 +146,17 @@ void weno_field(const kfvm_table* t, const Consts& k, const double* g, double* b
       beta = fma(k.scale[a], d * d, beta);
     }
     if (beta_out) beta_out[q] = beta;
-    wt[q] = t->gamma_lin[q] / fma(beta, beta, k.eps);  // P eq. nlinWts
+    // P eq. nlinWts: gamma_q / (beta_q^2 + eps), evaluated as gamma_q * (1 / d)
+    wt[q] = t->gamma_lin[q] * (1.0 / fma(beta, beta, k.eps));
   }
   double sum = wt[0];
   for (int q = 1; q < NS; ++q) sum = sum + wt[q];
+  const double inv_sum = 1.0 / sum;
   double om[KFVM_MAX_STENCILS] = {0};
-  for (int q = 0; q < NS; ++q) om[q] = wt[q] / sum;
+  for (int q = 0; q < NS; ++q) om[q] = wt[q] * inv_sum;
   if (omega_out)
     for (int q = 0; q < NS; ++q) omega_out[q] = om[q];
-  c[0] = om[0] / t->gamma_lin[0];
+  c[0] = om[0] * (1.0 / t->gamma_lin[0]);
   for (int q = 1; q < NS; ++q) c[q] = fma(-c[0], t->gamma_lin[q], om[q]);
   for (int s = 0; s < t->n_points; ++s) {
     double v = 0.0;
@@ -214,12 +225,12 @@ int limit_cell(const Consts& k, int npts, double* st, const double* nbr, double*
   // pressure by bisection (P eqs. thetapRoot/thetaP)
   double thp = 1.0;
   for (int s = 0; s < npts; ++s) {
-    if (pressure(dim, st + s * nv, k.gm1) < pmin) {
+    if (p_below(dim, st + s * nv, k.gm1, pmin)) {
       double lo = 0.0, hi = 1.0, x[5];
       for (int it = 0; it < 100 && (hi - lo) > 1e-12 * hi; ++it) {
         const double mid = 0.5 * (lo + hi);
         for (int v = 0; v < nv; ++v) x[v] = fma(mid, st[s * nv + v] - Uc[v], Uc[v]);
-        if (pressure(dim, x, k.gm1) >= pmin)
+        if (!p_below(dim, x, k.gm1, pmin))
           lo = mid;
         else
           hi = mid;

@@ -33,7 +33,7 @@ namespace kfvm_b200 {
 #define KFVM_FAST_MINB 1
 #endif
 #ifndef KFVM_MMA_MINB
-#define KFVM_MMA_MINB 2
+#define KFVM_MMA_MINB 3
 #endif
 __constant__ DevConsts c_k;
 __constant__ DevTable c_t;
@@ -73,571 +73,7 @@ constexpr int full_size(int dim, int R) {
 }
 constexpr int npoints(int dim, int R) { return dim == 2 ? 4 * R : 6 * R * R; }
 
-// ---------------------------------------------------------------- k_states
-template <int DIM, int R>
-__global__ void __launch_bounds__(128) k_states(const double* __restrict__ U,
-                                                double* __restrict__ St, Geo g, Chunk ch,
-                                                int* __restrict__ err) {
-  constexpr int nv = DIM + 2;
-  constexpr int N0 = full_size(DIM, R);
-  constexpr int NP = npoints(DIM, R);
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= ch.next) return;
-  const int a = (int)(tid % ch.ex);
-  const long long r1 = tid / ch.ex;
-  const int b = (int)(r1 % ch.em);
-  const int c = (int)(r1 / ch.em);
-  const int x = a - 1;
-  const int j = DIM == 3 ? b - 1 : 0;
-  const int p = ch.c0 - 1 + c;
-
-  double Uc[nv];
-  const long long ic = uidx<DIM>(g, x, j, p);
-#pragma unroll
-  for (int v = 0; v < nv; ++v) Uc[v] = U[v * g.vstride + ic];
-  const DTransform T = d_make_transform(DIM, Uc);
-
-  long long cell[N0];
-  for (int h = 0; h < N0; ++h)
-    cell[h] = uidx<DIM>(g, x + c_t.off_x[h], j + c_t.off_m[h], p + c_t.off_p[h]);
-
-  double W[NP * nv];
-  double gv[N0];
-  const int NS = c_t.n_stencils;
-  for (int v = 0; v < nv; ++v) {
-    for (int h = 0; h < N0; ++h) {
-      double Uh[nv];
-#pragma unroll
-      for (int u = 0; u < nv; ++u) Uh[u] = U[u * g.vstride + cell[h]];
-      gv[h] = d_to_recon(DIM, T, c_k.gm1, Uh, v);
-    }
-    double wt[8], cq[8];
-    for (int q = 0; q < NS; ++q) {
-      const int N = c_t.size[q];
-      const int* gat = c_gather + c_t.cell_offset[q];
-      const double* D = c_t.deriv + (long long)c_t.cell_offset[q] * c_t.n_alpha;
-      double beta = 0.0;
-      for (int al = 0; al < c_t.n_alpha; ++al) {
-        double d = 0.0;
-        for (int h = 0; h < N; ++h) d = fma(__ldg(D + al * N + h), gv[gat[h]], d);
-        beta = fma(c_t.scale[al], d * d, beta);
-      }
-      wt[q] = c_t.gamma_lin[q] / fma(beta, beta, c_k.eps);
-    }
-    double sum = wt[0];
-    for (int q = 1; q < NS; ++q) sum = sum + wt[q];
-    double om[8];
-    for (int q = 0; q < NS; ++q) om[q] = wt[q] / sum;
-    cq[0] = om[0] / c_t.gamma_lin[0];
-    for (int q = 1; q < NS; ++q) cq[q] = fma(-cq[0], c_t.gamma_lin[q], om[q]);
-    for (int s = 0; s < NP; ++s) {
-      double val = 0.0;
-      for (int q = 0; q < NS; ++q) {
-        const int N = c_t.size[q];
-        const int* gat = c_gather + c_t.cell_offset[q];
-        const double* rr = c_t.face + (long long)c_t.cell_offset[q] * NP + (long long)s * N;
-        double pp = 0.0;
-        for (int h = 0; h < N; ++h) pp = fma(__ldg(rr + h), gv[gat[h]], pp);
-        val = (q == 0) ? cq[0] * pp : fma(cq[q], pp, val);
-      }
-      W[s * nv + v] = val;
-    }
-  }
-  double st[NP * nv];
-  for (int s = 0; s < NP; ++s) d_from_recon(DIM, T, c_k.inv_gm1, W + s * nv, st + s * nv);
-  constexpr int NN = DIM == 3 ? 27 : 9;
-  double nbr[NN * nv];
-  {
-    int m = 0;
-    const int kr = DIM == 3 ? 1 : 0;
-    for (int cc = -1; cc <= 1; ++cc)
-      for (int bb = -kr; bb <= kr; ++bb)
-        for (int aa = -1; aa <= 1; ++aa, ++m) {
-          // neighbourhood order: i fastest, then mid (3-D) / slab (2-D), then slab
-          int jj = j, pp = p;
-          if (DIM == 3) {
-            jj = j + bb;
-            pp = p + cc;
-          } else {
-            pp = p + cc;
-          }
-          const long long o = uidx<DIM>(g, x + aa, jj, pp);
-#pragma unroll
-          for (int v = 0; v < nv; ++v) nbr[m * nv + v] = U[v * g.vstride + o];
-        }
-  }
-  if (d_limit<DIM>(c_k, NP, st, nbr)) atomicOr(err, 2);
-  for (int s = 0; s < NP; ++s)
-#pragma unroll
-    for (int v = 0; v < nv; ++v) St[(long long)(s * nv + v) * ch.next + tid] = st[s * nv + v];
-}
-
-// Phi^-1, positivity limiter and store of the 32 cells of a CTA (cell = lane,
-// points s = wv + k*nv); shared by the reconstruction kernels.
-template <int D, int NP, int KP, int NRX, int NRM, int NRP, int NREG>
-__device__ __forceinline__ void limiter_epilogue(const double* __restrict__ U,
-                                                 double* __restrict__ St, const Geo& g,
-                                                 const Chunk& ch, int* __restrict__ err,
-                                                 const double* sW, const double* sT,
-                                                 const double* sN, double* sTh, int lane, int wv,
-                                                 bool active, int x, int j, int p, int a, int b,
-                                                 int c) {
-  constexpr int nv = D + 2;
-  const int rc0 = (1 * NRM + NRM / 2) * NRX + lane + 1;  // centre of this cell in the region
-  double rbmax = sN[rc0], rbmin = sN[rc0], pbmin = sN[NREG + rc0], cmin = sN[2 * NREG + rc0];
-#pragma unroll
-  for (int dz = 0; dz < NRP; ++dz)
-#pragma unroll
-    for (int dm = 0; dm < NRM; ++dm)
-#pragma unroll
-      for (int dx = 0; dx < 3; ++dx) {
-        const int r = (dz * NRM + dm) * NRX + lane + dx;
-        rbmax = fmax(rbmax, sN[r]);
-        rbmin = fmin(rbmin, sN[r]);
-        pbmin = fmin(pbmin, sN[NREG + r]);
-        cmin = fmin(cmin, sN[2 * NREG + r]);
-      }
-  double delta = 0.5 * (sN[3 * NREG + rc0 + 1] - sN[3 * NREG + rc0 - 1]);
-  if (D == 3) {
-    delta = fma(0.5, sN[4 * NREG + rc0 + NRX] - sN[4 * NREG + rc0 - NRX], delta);
-    delta = fma(0.5, sN[5 * NREG + rc0 + NRM * NRX] - sN[5 * NREG + rc0 - NRM * NRX], delta);
-  } else {
-    delta = fma(0.5, sN[4 * NREG + rc0 + NRX] - sN[4 * NREG + rc0 - NRX], delta);
-  }
-  const double kc = c_k.kf * cmin;
-  double eta = -(delta + kc) / kc;
-  eta = fmin(1.0, fmax(0.0, eta));
-  const double fup = fma(c_k.kappa, 1.0 - eta, 1.0);
-  const double flo = fma(-c_k.kappa, 1.0 - eta, 1.0);
-  const double rmax = rbmax * fup;
-  const double rmin = rbmin * flo;
-  const double pmin = pbmin * flo;
-  const double rt = sT[lane];
-  const double pt = sN[NREG + rc0];
-  if (!(rt > 0.0) || !(pt > 0.0) || !(rmin > 0.0) || !(pmin > 0.0)) {
-    if (active && wv == 0) atomicOr(err, 2);
-  }
-  DTransform T;
-  T.rt = rt;
-  T.ut[0] = sT[32 + lane];
-  T.ut[1] = sT[64 + lane];
-  T.ut[2] = sT[96 + lane];
-  T.ke = sT[128 + lane];
-  double Ubar[nv];
-  {
-    // the cell average itself (the limiter's convex-combination anchor)
-    const long long ic = uidx<D>(g, x, j, p);
-#pragma unroll
-    for (int v = 0; v < nv; ++v) Ubar[v] = __ldg(U + v * g.vstride + ic);
-  }
-  double st[KP][nv];
-  double th = 1.0;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    const int s = wv + k * nv;
-    if (s < NP) {
-      double Wp[nv];
-#pragma unroll
-      for (int v = 0; v < nv; ++v) Wp[v] = sW[(s * nv + v) * 32 + lane];
-      d_from_recon(D, T, c_k.inv_gm1, Wp, st[k]);
-      const double r = st[k][0];
-      if (r < rmin)
-        th = fmin(th, (rt - rmin) / (rt - r));
-      else if (r > rmax)
-        th = fmin(th, (rmax - rt) / (r - rt));
-    }
-  }
-  sTh[wv * 32 + lane] = th;
-  __syncthreads();
-  th = 1.0;
-#pragma unroll
-  for (int q = 0; q < nv; ++q) th = fmin(th, sTh[q * 32 + lane]);
-  if (th < 1.0) {
-#pragma unroll
-    for (int k = 0; k < KP; ++k)
-#pragma unroll
-      for (int v = 0; v < nv; ++v) st[k][v] = fma(th, st[k][v] - Ubar[v], Ubar[v]);
-  }
-  double thp = 1.0;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    const int s = wv + k * nv;
-    if (s < NP && d_pressure(D, st[k], c_k.gm1) < pmin) {
-      double lo = 0.0, hi = 1.0, xx[nv];
-      for (int it = 0; it < 100 && (hi - lo) > 1e-12 * hi; ++it) {
-        const double mid = 0.5 * (lo + hi);
-#pragma unroll
-        for (int v = 0; v < nv; ++v) xx[v] = fma(mid, st[k][v] - Ubar[v], Ubar[v]);
-        if (d_pressure(D, xx, c_k.gm1) >= pmin)
-          lo = mid;
-        else
-          hi = mid;
-      }
-      thp = fmin(thp, lo);
-    }
-  }
-  __syncthreads();
-  sTh[wv * 32 + lane] = thp;
-  __syncthreads();
-  thp = 1.0;
-#pragma unroll
-  for (int q = 0; q < nv; ++q) thp = fmin(thp, sTh[q * 32 + lane]);
-  if (!active) return;
-  const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    const int s = wv + k * nv;
-    if (s < NP) {
-#pragma unroll
-      for (int v = 0; v < nv; ++v) {
-        const double u = thp < 1.0 ? fma(thp, st[k][v] - Ubar[v], Ubar[v]) : st[k][v];
-        St[(long long)(s * nv + v) * ch.next + tid] = u;
-      }
-    }
-  }
-}
-
-// ----------------------------------------------------------- k_states_fast
-// One CTA = 32 consecutive extended cells along x; warp v reconstructs
-// variable v of those 32 cells (g in registers, unrolled contractions with
-// __constant__ weight operands from kfvm_gen.cuh).  The face values meet in
-// shared memory for Phi^-1 and the positivity limiter, which all 32*nv
-// threads share (cell = lane, points s = warp + k*nv).
-template <int D, int R, int V>
-__device__ __forceinline__ void gather_var(const double* __restrict__ U, long long vstride,
-                                           const int* xs, const long long* ms,
-                                           const long long* ps, const DTransform& T,
-                                           double* gv, int gstride) {
-  using G = Gen<D, R>;
-#pragma unroll
-  for (int h = 0; h < G::N0; ++h) {
-    const int ox = G::off(h, 0);
-    const int om = D == 3 ? G::off(h, 1) : 0;
-    const int op = D == 3 ? G::off(h, 2) : G::off(h, 1);
-    const long long idx = ps[op + R] + ms[om + R] + xs[ox + R];
-    if (V == 0) {
-      gv[h * gstride] = __ldg(U + idx);
-    } else if (V <= D) {
-      gv[h * gstride] = fma(-T.ut[V - 1], __ldg(U + idx), __ldg(U + V * vstride + idx)) * T.inv_r;
-    } else {
-      double t = fma(T.ke, __ldg(U + idx), __ldg(U + (D + 1) * vstride + idx));
-      t = fma(-T.ut[0], __ldg(U + vstride + idx), t);
-      t = fma(-T.ut[1], __ldg(U + 2 * vstride + idx), t);
-      if (D == 3) t = fma(-T.ut[2], __ldg(U + 3 * vstride + idx), t);
-      gv[h * gstride] = c_k.gm1 * t;
-    }
-  }
-}
-
-template <int D, int R>
-__global__ void __launch_bounds__(32 * (D + 2), KFVM_FAST_MINB) k_states_fast(const double* __restrict__ U,
-                                                              double* __restrict__ St, Geo g,
-                                                              Chunk ch, int* __restrict__ err) {
-  using G = Gen<D, R>;
-  constexpr int nv = D + 2, NP = G::NP, N0 = G::N0;
-  constexpr int NRX = 34, NRM = D == 3 ? 3 : 1, NRP = 3;
-  constexpr int NREG = NRX * NRM * NRP;
-  constexpr int KP = (NP + nv - 1) / nv;
-  constexpr int NT = 32 * nv;
-  constexpr int GW = N0 * NT > NP * nv * 32 ? N0 * NT : NP * nv * 32;
-  extern __shared__ double smem[];
-  double* sG = smem;       // [h][thread]   stencil values of each (cell, var)
-  double* sW = smem;       // [s][v][cell]  face values (aliases sG after a barrier)
-  double* sN = smem + GW;  // neighbourhood region quantities
-  double* sT = sN + 6 * NREG;
-  double* sTh = sT + 5 * 32;
-
-  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
-  const int nseg = (ch.ex + 31) >> 5;
-  int bid = blockIdx.x;
-  const int seg = bid % nseg;
-  bid /= nseg;
-  const int b = bid % ch.em;
-  const int c = bid / ch.em;
-  const int a0 = seg * 32;
-  const int a = a0 + lane;
-  const bool active = a < ch.ex;
-  const int x = a - 1, j = D == 3 ? b - 1 : 0, p = ch.c0 - 1 + c;
-
-  // ---- phase A: reconstruction of variable wv for cell `lane`
-  {
-    int xs[2 * R + 1];
-    long long ms[2 * R + 1], ps[2 * R + 1];
-#pragma unroll
-    for (int k = 0; k <= 2 * R; ++k) {
-      xs[k] = remap(x + k - R, g.nx, c_k.bc);
-      ms[k] = D == 3 ? (long long)remap(j + k - R, g.nm, c_k.bc) * g.nx : 0;
-      ps[k] = (long long)(p + k - R + g.H) * g.pstride;
-    }
-    double Uc[nv];
-    const long long ic = ps[R] + ms[R] + xs[R];
-#pragma unroll
-    for (int v = 0; v < nv; ++v) Uc[v] = __ldg(U + v * g.vstride + ic);
-    const DTransform T = d_make_transform(D, Uc);
-    double* gv = sG + threadIdx.x;
-    switch (wv) {
-      case 0: gather_var<D, R, 0>(U, g.vstride, xs, ms, ps, T, gv, NT); break;
-      case 1: gather_var<D, R, 1>(U, g.vstride, xs, ms, ps, T, gv, NT); break;
-      case 2: gather_var<D, R, 2>(U, g.vstride, xs, ms, ps, T, gv, NT); break;
-      case 3: gather_var<D, R, 3>(U, g.vstride, xs, ms, ps, T, gv, NT); break;
-      default: gather_var<D, R, D == 3 ? 4 : 3>(U, g.vstride, xs, ms, ps, T, gv, NT); break;
-    }
-    double w[NP];
-    G::weno(gv, NT, w, 1, c_t.scale, c_t.gamma_lin, c_k.eps, c_gather);
-    __syncthreads();  // sW aliases sG
-#pragma unroll
-    for (int s = 0; s < NP; ++s) sW[(s * nv + wv) * 32 + lane] = w[s];
-    if (wv == 0) {
-      sT[0 * 32 + lane] = T.rt;
-      sT[1 * 32 + lane] = T.ut[0];
-      sT[2 * 32 + lane] = T.ut[1];
-      sT[3 * 32 + lane] = T.ut[2];
-      sT[4 * 32 + lane] = T.ke;
-    }
-  }
-  // ---- phase B: averages-derived quantities of the 3^d neighbourhood region
-  for (int r = threadIdx.x; r < NREG; r += 32 * nv) {
-    const int rx = r % NRX, rr = r / NRX, rm = rr % NRM, rp = rr / NRM;
-    const long long o = uidx<D>(g, x - lane - 1 + rx, j + rm - NRM / 2, p + rp - 1);
-    double Ur[nv];
-#pragma unroll
-    for (int v = 0; v < nv; ++v) Ur[v] = __ldg(U + v * g.vstride + o);
-    const double pr = d_pressure(D, Ur, c_k.gm1);
-    sN[0 * NREG + r] = Ur[0];
-    sN[1 * NREG + r] = pr;
-    sN[2 * NREG + r] = d_sound(c_k.gamma, pr, Ur[0]);
-#pragma unroll
-    for (int d = 0; d < D; ++d) sN[(3 + d) * NREG + r] = Ur[1 + d] / Ur[0];
-  }
-  __syncthreads();
-  limiter_epilogue<D, NP, KP, NRX, NRM, NRP, NREG>(U, St, g, ch, err, sW, sT, sN, sTh, lane, wv,
-                                                   active, x, j, p, a, b, c);
-}
-
-// ------------------------------------------------------------ k_states_mma
-// Stencil contractions on the FP64 tensor cores.  mma.sync.m8n8k4.f64 was
-// measured bit-identical to the sequential chain fma(a3,b3,fma(a2,b2,fma(a1,
-// b1,fma(a0,b0,c)))) (tools/ubench/dmma_rounding.cu), and a zero-weight term
-// is exactly neutral for an accumulator started at +0.0 (it can never become
-// -0.0), so contracting the zero-padded 4-wide chunks of every stencil on
-// DMMA reproduces the oracle's stencil-order fma chains bit for bit.
-//
-// CTA = 32 consecutive extended cells x nv warps; warp v owns variable v.
-//   A (8 cells x 4 stencil entries) from shared memory sG[v][h][cell],
-//   B (4 entries x 8 columns) = weights in fragment order (global, L1),
-//   pass 1: derivative columns -> beta_q;  pass 2: face-point columns,
-//   combined into the WENO-AO value with c_q after each stencil.
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
-}
-
-template <int D, int R>
-struct MmaCfg {
-  using G = Gen<D, R>;
-  static constexpr int nv = D + 2;
-  static constexpr int RS = 36;                    // padded row of 32 cells
-  static constexpr int ND = (G::NA + 7) / 8;       // derivative column tiles
-  static constexpr int NPT = (G::NP + 7) / 8;      // face-point column tiles
-  static constexpr int NREG = 34 * (D == 3 ? 3 : 1) * 3;
-  static constexpr int SG = nv * G::N0 * RS;       // stencil values
-  static constexpr int SWW = G::NP * nv * 32;      // face values (aliases sG)
-  static constexpr int SGW = SG > SWW ? SG : SWW;
-  static constexpr int SD = nv * 8 * ND * RS;      // derivative tiles
-  static constexpr int SC = nv * G::NS * RS;       // c_q per (var, cell)
-  static constexpr size_t bytes() {
-    return sizeof(double) * (SGW + SD + SC + 6 * NREG + 5 * 32 + nv * 32) +
-           sizeof(int) * 4 * G::NCHUNK;
-  }
-};
-
-template <int D, int R>
-__global__ void __launch_bounds__(32 * (D + 2), KFVM_MMA_MINB) k_states_mma(
-    const double* __restrict__ U, double* __restrict__ St, Geo g, Chunk ch,
-    int* __restrict__ err, const double* __restrict__ Bd, const double* __restrict__ Bf,
-    const int* __restrict__ gat4) {
-  using G = Gen<D, R>;
-  using M = MmaCfg<D, R>;
-  constexpr int nv = D + 2, NP = G::NP, N0 = G::N0, RS = M::RS, ND = M::ND, NPT = M::NPT;
-  constexpr int NRX = 34, NRM = D == 3 ? 3 : 1, NRP = 3;
-  constexpr int NREG = M::NREG;
-  constexpr int KP = (NP + nv - 1) / nv;
-  extern __shared__ double smem[];
-  double* sG = smem;
-  double* sW = smem;
-  double* sD = smem + M::SGW;
-  double* sC = sD + M::SD;
-  double* sN = sC + M::SC;
-  double* sT = sN + 6 * NREG;
-  double* sTh = sT + 5 * 32;
-  int* sGat = reinterpret_cast<int*>(sTh + nv * 32);
-
-  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 4 * G::NCHUNK; i += 32 * nv) sGat[i] = gat4[i];
-  const int nseg = (ch.ex + 31) >> 5;
-  int bid = blockIdx.x;
-  const int seg = bid % nseg;
-  bid /= nseg;
-  const int b = bid % ch.em;
-  const int c = bid / ch.em;
-  const int a0 = seg * 32;
-  const int a = a0 + lane;
-  const bool active = a < ch.ex;
-  const int x = a - 1, j = D == 3 ? b - 1 : 0, p = ch.c0 - 1 + c;
-
-  // ---- phase A: transformed stencil values of (cell = lane, var = wv)
-  double* sGv = sG + wv * N0 * RS;
-  {
-    int xs[2 * R + 1];
-    long long ms[2 * R + 1], ps[2 * R + 1];
-#pragma unroll
-    for (int k = 0; k <= 2 * R; ++k) {
-      xs[k] = remap(x + k - R, g.nx, c_k.bc);
-      ms[k] = D == 3 ? (long long)remap(j + k - R, g.nm, c_k.bc) * g.nx : 0;
-      ps[k] = (long long)(p + k - R + g.H) * g.pstride;
-    }
-    double Uc[nv];
-    const long long ic = ps[R] + ms[R] + xs[R];
-#pragma unroll
-    for (int v = 0; v < nv; ++v) Uc[v] = __ldg(U + v * g.vstride + ic);
-    const DTransform T = d_make_transform(D, Uc);
-    double* gv = sGv + lane;
-    switch (wv) {
-      case 0: gather_var<D, R, 0>(U, g.vstride, xs, ms, ps, T, gv, RS); break;
-      case 1: gather_var<D, R, 1>(U, g.vstride, xs, ms, ps, T, gv, RS); break;
-      case 2: gather_var<D, R, 2>(U, g.vstride, xs, ms, ps, T, gv, RS); break;
-      case 3: gather_var<D, R, 3>(U, g.vstride, xs, ms, ps, T, gv, RS); break;
-      default: gather_var<D, R, D == 3 ? 4 : 3>(U, g.vstride, xs, ms, ps, T, gv, RS); break;
-    }
-    if (wv == 0) {
-      sT[0 * 32 + lane] = T.rt;
-      sT[1 * 32 + lane] = T.ut[0];
-      sT[2 * 32 + lane] = T.ut[1];
-      sT[3 * 32 + lane] = T.ut[2];
-      sT[4 * 32 + lane] = T.ke;
-    }
-  }
-  __syncthreads();  // sGat visible, sG complete
-  const int k4 = lane & 3, r8 = lane >> 2;
-  // ---- pass 1: derivative columns -> beta_q (thread = cell `lane`)
-  double* sDv = sD + wv * 8 * ND * RS;
-  double* sCv = sC + wv * G::NS * RS;
-  double beta[G::NS];
-#pragma unroll
-  for (int q = 0; q < G::NS; ++q) {
-    double acc[4][ND][2];
-#pragma unroll
-    for (int m = 0; m < 4; ++m)
-#pragma unroll
-      for (int n = 0; n < ND; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-#pragma unroll 2
-    for (int jj = 0; jj < G::kc(q); ++jj) {
-      const int ck = G::cbase(q) + jj;
-      const double* gr = sGv + sGat[ck * 4 + k4] * RS + r8;
-      double av[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) av[m] = gr[8 * m];
-#pragma unroll
-      for (int n = 0; n < ND; ++n) {
-        const double bv = __ldg(Bd + (ck * ND + n) * 32 + lane);
-#pragma unroll
-        for (int m = 0; m < 4; ++m) dmma(acc[m][n][0], acc[m][n][1], av[m], bv);
-      }
-    }
-    // acc[m][n][e]: cell 8m + r8, alpha 8n + 2*k4 + e
-#pragma unroll
-    for (int m = 0; m < 4; ++m)
-#pragma unroll
-      for (int n = 0; n < ND; ++n)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) sDv[(8 * n + 2 * k4 + e) * RS + 8 * m + r8] = acc[m][n][e];
-    __syncwarp();
-    double bq = 0.0;
-#pragma unroll
-    for (int al = 0; al < G::NA; ++al) {
-      const double d = sDv[al * RS + lane];
-      bq = fma(c_t.scale[al], d * d, bq);
-    }
-    beta[q] = bq;
-    __syncwarp();
-  }
-  {
-    double om[G::NS];
-#pragma unroll
-    for (int q = 0; q < G::NS; ++q) om[q] = c_t.gamma_lin[q] / fma(beta[q], beta[q], c_k.eps);
-    double sum = om[0];
-#pragma unroll
-    for (int q = 1; q < G::NS; ++q) sum = sum + om[q];
-#pragma unroll
-    for (int q = 0; q < G::NS; ++q) om[q] = om[q] / sum;
-    const double c0 = om[0] / c_t.gamma_lin[0];
-    sCv[lane] = c0;
-#pragma unroll
-    for (int q = 1; q < G::NS; ++q) sCv[q * RS + lane] = fma(-c0, c_t.gamma_lin[q], om[q]);
-  }
-  __syncwarp();
-  // ---- pass 2: face-point columns, WENO-AO combination per stencil
-  double V[4][NPT][2];
-#pragma unroll
-  for (int q = 0; q < G::NS; ++q) {
-    double acc[4][NPT][2];
-#pragma unroll
-    for (int m = 0; m < 4; ++m)
-#pragma unroll
-      for (int n = 0; n < NPT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-#pragma unroll 2
-    for (int jj = 0; jj < G::kc(q); ++jj) {
-      const int ck = G::cbase(q) + jj;
-      const double* gr = sGv + sGat[ck * 4 + k4] * RS + r8;
-      double av[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) av[m] = gr[8 * m];
-#pragma unroll
-      for (int n = 0; n < NPT; ++n) {
-        const double bv = __ldg(Bf + (ck * NPT + n) * 32 + lane);
-#pragma unroll
-        for (int m = 0; m < 4; ++m) dmma(acc[m][n][0], acc[m][n][1], av[m], bv);
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const double cq = sCv[q * RS + 8 * m + r8];
-#pragma unroll
-      for (int n = 0; n < NPT; ++n)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          V[m][n][e] = q == 0 ? cq * acc[m][n][e] : fma(cq, acc[m][n][e], V[m][n][e]);
-    }
-  }
-  __syncthreads();  // sW aliases sG
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-#pragma unroll
-    for (int n = 0; n < NPT; ++n)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int sp = 8 * n + 2 * k4 + e;
-        if (sp < NP) sW[(sp * nv + wv) * 32 + 8 * m + r8] = V[m][n][e];
-      }
-  // ---- phase B: averages-derived quantities of the 3^d neighbourhood region
-  for (int r = threadIdx.x; r < NREG; r += 32 * nv) {
-    const int rx = r % NRX, rr = r / NRX, rm = rr % NRM, rp = rr / NRM;
-    const long long o = uidx<D>(g, x - lane - 1 + rx, j + rm - NRM / 2, p + rp - 1);
-    double Ur[nv];
-#pragma unroll
-    for (int v = 0; v < nv; ++v) Ur[v] = __ldg(U + v * g.vstride + o);
-    const double pr = d_pressure(D, Ur, c_k.gm1);
-    sN[0 * NREG + r] = Ur[0];
-    sN[1 * NREG + r] = pr;
-    sN[2 * NREG + r] = d_sound(c_k.gamma, pr, Ur[0]);
-#pragma unroll
-    for (int d = 0; d < D; ++d) sN[(3 + d) * NREG + r] = Ur[1 + d] / Ur[0];
-  }
-  __syncthreads();
-  limiter_epilogue<D, NP, KP, NRX, NRM, NRP, NREG>(U, St, g, ch, err, sW, sT, sN, sTh, lane, wv,
-                                                   active, x, j, p, a, b, c);
-}
+#include "kfvm_recon.cuh"
 
 // ------------------------------------------------------------------ k_flux
 template <int DIM>
@@ -932,6 +368,7 @@ struct kfvm_handle {
   int nsa = 0, p0 = 0, rank = 0, nranks = 1, device = 0;
   Geo g{};
   double *U0 = nullptr, *Ua = nullptr, *Ub = nullptr;
+  double* Pr = nullptr;  // k_prims output: p, c, 1/rho, u_d per cell (incl. halos)
   double *St = nullptr, *F = nullptr, *aos = nullptr;
   size_t st_elems = 0, f_elems = 0, aos_elems = 0;
   int chunk = 0;
@@ -999,38 +436,24 @@ void toc(kfvm_handle* h, double* acc) {
   *acc += ms;
 }
 
-template <int D, int R>
-size_t fast_smem() {
-  using G = Gen<D, R>;
-  constexpr int nv = D + 2, NT = 32 * nv;
-  constexpr int GW = G::N0 * NT > G::NP * nv * 32 ? G::N0 * NT : G::NP * nv * 32;
-  constexpr int NREG = 34 * (D == 3 ? 3 : 1) * 3;
-  return sizeof(double) * (GW + 6 * NREG + 5 * 32 + nv * 32);
-}
-
-template <int D, int R>
-void set_fast_smem() {
-  cudaFuncSetAttribute(k_states_fast<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)fast_smem<D, R>());
-}
-
 template <int DIM, int R>
 void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   tic(h);
+  const long long nblk = (long long)((ch.ex + 31) / 32) * ch.em * ch.ep;
   if constexpr (!(DIM == 3 && R == 3)) {
     if (h->engine == 2) {
-      const long long nblk = (long long)((ch.ex + 31) / 32) * ch.em * ch.ep;
       k_states_mma<DIM, R><<<(unsigned)nblk, 32 * (DIM + 2), MmaCfg<DIM, R>::bytes(), h->stream>>>(
-          U, h->St, h->g, ch, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4);
+          U, h->Pr, h->St, h->g, ch, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4);
     } else if (h->engine == 1) {
-      const long long nblk = (long long)((ch.ex + 31) / 32) * ch.em * ch.ep;
-      k_states_fast<DIM, R><<<(unsigned)nblk, 32 * (DIM + 2), fast_smem<DIM, R>(), h->stream>>>(
-          U, h->St, h->g, ch, h->d_err);
+      k_states_fast<DIM, R><<<(unsigned)nblk, 32 * (DIM + 2), 0, h->stream>>>(U, h->Pr, h->St, h->g,
+                                                                            ch, h->d_err);
     } else {
-      k_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->St, h->g, ch, h->d_err);
+      k_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
+                                                                    h->d_err);
     }
   } else {
-    k_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->St, h->g, ch, h->d_err);
+    k_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
+                                                                  h->d_err);
   }
   h->launches++;
   toc(h, &h->t_states);
@@ -1111,9 +534,21 @@ int reduce_smax(kfvm_handle* h) {
 }
 
 // one stage: halo, then per chunk states -> flux -> update
+void prims(kfvm_handle* h, const double* U) {
+  const long long n = h->g.vstride;
+  tic(h);
+  if (h->dim == 2)
+    k_prims<2><<<blocks(n, 256), 256, 0, h->stream>>>(U, h->Pr, n, h->g.vstride);
+  else
+    k_prims<3><<<blocks(n, 256), 256, 0, h->stream>>>(U, h->Pr, n, h->g.vstride);
+  h->launches++;
+  toc(h, &h->t_other);
+}
+
 int run_stage(kfvm_handle* h, const double* Uin, double* Uout, int stage) {
   int rc = halo(h, const_cast<double*>(Uin));
   if (rc) return rc;
+  prims(h, Uin);
   for (int c0 = 0; c0 < h->g.np_loc; c0 += h->chunk) {
     const Chunk ch = make_chunk(h, c0, std::min(h->chunk, h->g.np_loc - c0));
     states_and_flux(h, Uin, ch);
@@ -1200,21 +635,8 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   for (int i = 0; i < G::NTOT; ++i)
     if (t->gather[i] != G::GATHER[i])
       return fail(h, KFVM_ERR_CONFIG, "table substencils differ from kfvm_gen.cuh");
-  // transposed copies ([q][h][s] and [q][h][a], rows padded to NAP): the
-  // values are the table's bytes, only the order changes
-  std::vector<double> ft((size_t)G::NTOT * G::NP), dt((size_t)G::NTOT * G::NAP, 0.0);
-  for (int q = 0; q < G::NS; ++q) {
-    const int N = t->size[q], o = t->cell_offset[q];
-    for (int hh = 0; hh < N; ++hh) {
-      for (int sp = 0; sp < G::NP; ++sp)
-        ft[(size_t)(o + hh) * G::NP + sp] = t->face[(size_t)o * G::NP + (size_t)sp * N + hh];
-      for (int a = 0; a < G::NA; ++a)
-        dt[(size_t)(o + hh) * G::NAP + a] = t->deriv[(size_t)o * G::NA + (size_t)a * N + hh];
-    }
-  }
-  CK(cudaMemcpyToSymbol(G::face_symbol(), ft.data(), sizeof(double) * ft.size()));
-  CK(cudaMemcpyToSymbol(G::deriv_symbol(), dt.data(), sizeof(double) * dt.size()));
-  set_fast_smem<D, R>();
+  CK(cudaMemcpyToSymbol(G::face_symbol(), t->face, sizeof(double) * G::NTOT * G::NP));
+  CK(cudaMemcpyToSymbol(G::deriv_symbol(), t->deriv, sizeof(double) * G::NTOT * G::NA));
   // DMMA operands: per 4-entry chunk of each stencil (zero-padded at the
   // front), B fragments in lane order (k = lane%4, column = lane/4) and the
   // S0 position of every chunk slot
@@ -1284,6 +706,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   h->R = cfg->radius;
   h->nv = cfg->dim + 2;
   h->NP = t->n_points;
+  h->engine = cfg->dim == 3 ? 2 : 1;  // DMMA for 3-D, unrolled DFMA for 2-D (measured)
   if (dist) {
     h->rank = dist->rank;
     h->nranks = dist->nranks;
@@ -1344,6 +767,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     T.cell_offset[q] = t->cell_offset[q];
     T.gamma_lin[q] = t->gamma_lin[q];
   }
+  T.inv_g0 = 1.0 / t->gamma_lin[0];
   for (int hh = 0; hh < t->n_full; ++hh) {
     T.off_x[hh] = t->offsets[3 * hh];
     if (cfg->dim == 3) {
@@ -1391,6 +815,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   bad(cudaMalloc(&h->U0, ufull * sizeof(double)), "cudaMalloc U0");
   bad(cudaMalloc(&h->Ua, ufull * sizeof(double)), "cudaMalloc Ua");
   bad(cudaMalloc(&h->Ub, ufull * sizeof(double)), "cudaMalloc Ub");
+  bad(cudaMalloc(&h->Pr, (size_t)h->g.vstride * (cfg->dim + 3) * sizeof(double)), "cudaMalloc prims");
   if (rc == KFVM_OK) {
     bad(cudaMemset(h->U0, 0, ufull * sizeof(double)), "memset");
     bad(cudaMemset(h->Ua, 0, ufull * sizeof(double)), "memset");
@@ -1451,7 +876,7 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
   if (!h) return;
   if (h->graph) cudaGraphExecDestroy(h->graph);
   if (h->comm) nccl().CommDestroy(h->comm);
-  for (void* p : {(void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->St, (void*)h->F,
+  for (void* p : {(void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
                   (void*)h->aos, (void*)h->d_face, (void*)h->d_deriv, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
                   (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4})
@@ -1517,6 +942,7 @@ extern "C" int kfvm_gpu_rhs(kfvm_handle* h, double* dUdt_host) {
 extern "C" int kfvm_gpu_states(kfvm_handle* h, double* states_host) {
   int rc = halo(h, h->U0);
   if (rc) return rc;
+  prims(h, h->U0);
   const long long per_cell = (long long)h->NP * h->nv;
   const long long plane_cells = h->g.pstride;
   double* dbuf = nullptr;
@@ -1586,7 +1012,7 @@ extern "C" int kfvm_gpu_run_async(kfvm_handle* h, int nsteps) {
   long long per_step = 0;
   {
     const int nchunks = (h->g.np_loc + h->chunk - 1) / h->chunk;
-    per_step = 1 + 3 * (1 + 3LL * nchunks);
+    per_step = 1 + 3 * (2 + 3LL * nchunks);
   }
   for (int s = 0; s < nsteps; ++s) CK(cudaGraphLaunch(h->graph, h->stream));
   h->launches += per_step * nsteps;

@@ -79,8 +79,8 @@ def gen_case(dim, R):
     tag = f"{dim}{R}"
     L = []
     L.append(f"// ---- dim={dim} R={R}: N0={len(full)} sizes={sizes} n_alpha={na} n_points={npnt}")
-    L.append(f"__constant__ __align__(16) double c_f{tag}[{total * npnt}];  // table.face transposed, [q][h][s]")
-    L.append(f"__constant__ __align__(16) double c_d{tag}[{total * (na + (na & 1))}];  // table.deriv, [q][h][a] padded")
+    L.append(f"__constant__ __align__(16) double c_f{tag}[{total * npnt}];  // table.face, [q][s][h]")
+    L.append(f"__constant__ __align__(16) double c_d{tag}[{total * na}];  // table.deriv, [q][a][h]")
     L.append(f"template <> struct Gen<{dim}, {R}> {{")
     L.append(f"  static constexpr int N0 = {len(full)}, NP = {npnt}, NA = {na}, NS = {ns}, NTOT = {total};")
     L.append(f"  static constexpr int OFF[{len(full)}][3] = {{" +
@@ -100,81 +100,52 @@ def gen_case(dim, R):
     L.append(f"  static constexpr int NCHUNK = {sum((n + 3) // 4 for n in sizes)};")
     L.append("  static const void* face_symbol() { return (const void*)&c_f%s; }" % tag)
     L.append("  static const void* deriv_symbol() { return (const void*)&c_d%s; }" % tag)
-    # WENO body, outer-product form: for each stencil q loop over its cells h
-    # (runtime loop) and update NA (derivatives) or NP (face points)
-    # independent accumulators per step -> ILP NA / NP, tiny code.  Weights are
-    # stored transposed, [q][h][a] and [q][h][s], so one h row is contiguous
-    # (LDCU.128).  Every dot product still accumulates over h in stencil
-    # order from 0.0 (the pinned FP contract).
-    nap = na + (na & 1)
-    L.append(f"  static constexpr int NAP = {nap};  // padded derivative row")
-    L.append("  // g of this thread lives in shared memory: g[h] = sg[h * gstride]")
-    L.append("  static __device__ __forceinline__ void weno(const double* sg, int gstride, double* sw,")
-    L.append("                                              int sstride, const double* __restrict__ sc,")
+    # WENO body, fully unrolled: stencil values in registers, every weight a
+    # __constant__ operand with a literal offset (table layouts [q][a][h] and
+    # [q][s][h]); each dot product is the stencil-order fma chain from 0.0.
+    L.append("  // beta_q, omega_q, WENO-AO values of one scalar field g on S0")
+    L.append("  static __device__ __forceinline__ void weno(const double (&g)[%d], double (&w)[%d],"
+             % (len(full), npnt))
+    L.append("                                              const double* __restrict__ sc,")
     L.append("                                              const double* __restrict__ gam, double eps,")
-    L.append("                                              const int* __restrict__ gat) {")
+    L.append("                                              double inv_g0) {")
     for q in range(ns):
-        L.append(f"    double b{q};")
-    for q in range(ns):
-        N, o = sizes[q], offs[q]
+        m, N, o = members[q], sizes[q], offs[q]
+        L.append(f"    double wt{q};")
         L.append("    {")
-        L.append(f"      double d[{nap}];")
-        L.append("#pragma unroll")
-        L.append(f"      for (int a = 0; a < {nap}; ++a) d[a] = 0.0;")
-        L.append("#pragma unroll 1")
-        L.append(f"      for (int h = 0; h < {N}; ++h) {{")
-        L.append(f"        const double gh = sg[gat[{o} + h] * gstride];")
-        L.append(f"        const double2* W = reinterpret_cast<const double2*>(c_d{tag} + ({o} + h) * {nap});")
-        L.append("#pragma unroll")
-        L.append(f"        for (int a = 0; a < {nap // 2}; ++a) {{")
-        L.append("          const double2 w2 = W[a];")
-        L.append("          d[2 * a] = fma(w2.x, gh, d[2 * a]);")
-        if na % 2:
-            L.append(f"          if (2 * a + 1 < {na}) d[2 * a + 1] = fma(w2.y, gh, d[2 * a + 1]);")
-        else:
-            L.append("          d[2 * a + 1] = fma(w2.y, gh, d[2 * a + 1]);")
-        L.append("        }")
-        L.append("      }")
-        L.append(f"      b{q} = 0.0;")
-        L.append("#pragma unroll")
-        L.append(f"      for (int a = 0; a < {na}; ++a) b{q} = fma(sc[a], d[a] * d[a], b{q});")
+        L.append("      double b = 0.0;")
+        for a in range(na):
+            base = o * na + a * N
+            L.append("      {")
+            L.append("        double d = 0.0;")
+            for hh, h in enumerate(m):
+                L.append(f"        d = fma(c_d{tag}[{base + hh}], g[{h}], d);")
+            L.append(f"        b = fma(sc[{a}], d * d, b);")
+            L.append("      }")
+        L.append(f"      wt{q} = gam[{q}] * (1.0 / fma(b, b, eps));")
         L.append("    }")
-    L.append(f"    double om[{ns}];")
+    L.append("    double sum = wt0;")
+    for q in range(1, ns):
+        L.append(f"    sum = sum + wt{q};")
+    L.append("    const double inv_sum = 1.0 / sum;")
     for q in range(ns):
-        L.append(f"    om[{q}] = gam[{q}] / fma(b{q}, b{q}, eps);")
-    L.append("    double sum = om[0];")
-    L.append("#pragma unroll")
-    L.append(f"    for (int q = 1; q < {ns}; ++q) sum = sum + om[q];")
-    L.append("#pragma unroll")
-    L.append(f"    for (int q = 0; q < {ns}; ++q) om[q] = om[q] / sum;")
-    L.append("    const double c0 = om[0] / gam[0];")
-    L.append(f"    double v[{npnt}];")
-    for q in range(ns):
-        N, o = sizes[q], offs[q]
+        L.append(f"    const double om{q} = wt{q} * inv_sum;")
+    L.append("    const double c0 = om0 * inv_g0;")
+    for q in range(1, ns):
+        L.append(f"    const double c{q} = fma(-c0, gam[{q}], om{q});")
+    for s_ in range(npnt):
         L.append("    {")
-        L.append(f"      const double c = {'c0' if q == 0 else f'fma(-c0, gam[{q}], om[{q}])'};")
-        L.append(f"      double p[{npnt}];")
-        L.append("#pragma unroll")
-        L.append(f"      for (int s = 0; s < {npnt}; ++s) p[s] = 0.0;")
-        L.append("#pragma unroll 1")
-        L.append(f"      for (int h = 0; h < {N}; ++h) {{")
-        L.append(f"        const double gh = sg[gat[{o} + h] * gstride];")
-        L.append(f"        const double2* W = reinterpret_cast<const double2*>(c_f{tag} + ({o} + h) * {npnt});")
-        L.append("#pragma unroll")
-        L.append(f"        for (int s = 0; s < {npnt // 2}; ++s) {{")
-        L.append("          const double2 w2 = W[s];")
-        L.append("          p[2 * s] = fma(w2.x, gh, p[2 * s]);")
-        L.append("          p[2 * s + 1] = fma(w2.y, gh, p[2 * s + 1]);")
-        L.append("        }")
-        L.append("      }")
-        L.append("#pragma unroll")
-        if q == 0:
-            L.append(f"      for (int s = 0; s < {npnt}; ++s) v[s] = c * p[s];")
-        else:
-            L.append(f"      for (int s = 0; s < {npnt}; ++s) v[s] = fma(c, p[s], v[s]);")
+        for q in range(ns):
+            m, N, o = members[q], sizes[q], offs[q]
+            base = o * npnt + s_ * N
+            L.append(f"      double p{q} = 0.0;")
+            for hh, h in enumerate(m):
+                L.append(f"      p{q} = fma(c_f{tag}[{base + hh}], g[{h}], p{q});")
+        L.append("      double v = c0 * p0;")
+        for q in range(1, ns):
+            L.append(f"      v = fma(c{q}, p{q}, v);")
+        L.append(f"      w[{s_}] = v;")
         L.append("    }")
-    L.append("#pragma unroll")
-    L.append(f"    for (int s = 0; s < {npnt}; ++s) sw[s * sstride] = v[s];")
     L.append("  }")
     L.append("};")
     return "\n".join(L)
