@@ -642,11 +642,12 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   // S0 position of every chunk slot
   using M = MmaCfg<D, R>;
   std::vector<double> bd((size_t)G::NCHUNK * M::ND * 32, 0.0), bf((size_t)G::NCHUNK * M::NPT * 32, 0.0);
-  std::vector<int> g4((size_t)G::NCHUNK * 4, 0);
+  std::vector<int> g4((size_t)G::NCHUNK * 5, 0);  // gather rows, then sQ (stencil | last<<8)
   for (int q = 0, ck = 0; q < G::NS; ++q) {
     const int N = t->size[q], o = t->cell_offset[q];
     const int kcq = (N + 3) / 4, pad = 4 * kcq - N;
     for (int jj = 0; jj < kcq; ++jj, ++ck) {
+      g4[(size_t)G::NCHUNK * 4 + ck] = q | (jj == kcq - 1 ? 256 : 0);
       for (int k = 0; k < 4; ++k) {
         const int hh = 4 * jj + k - pad;
         g4[(size_t)ck * 4 + k] = t->gather[o + (hh < 0 ? 0 : hh)];
