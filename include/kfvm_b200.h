@@ -184,6 +184,10 @@ int kfvm_gpu_step(kfvm_handle* h, double* dt_out);
 /* nsteps SSP-RK3 steps (CUDA-graph captured); dt_seq[nsteps] may be NULL.
  * Replaces advance_to for a fixed step count. */
 int kfvm_gpu_run(kfvm_handle* h, int nsteps, double* dt_seq);
+/* advance_to with fixed-CFL steps: step until t = t_final (the last
+ * step is clipped to land on it) or max_steps. */
+int kfvm_gpu_advance_to(kfvm_handle* h, double t_final, int max_steps, int* steps,
+                        double* t_reached);
 /* Asynchronous variant on the handle's stream; kfvm_gpu_sync waits and
  * reports device-side errors. */
 int kfvm_gpu_run_async(kfvm_handle* h, int nsteps);

@@ -90,7 +90,7 @@ inline double sound(double gamma, double p, double rho) {
 }
 
 struct Transform {  // Phi / Phi^-1 at the central average
-  double rt, inv_r, ut[3], ke;
+  double rt, inv_r, ut[3], mt[3], ke;
 };
 
 inline Transform make_transform(int dim, const double* Ur) {
@@ -98,7 +98,11 @@ inline Transform make_transform(int dim, const double* Ur) {
   T.rt = Ur[0];
   T.inv_r = 1.0 / Ur[0];
   T.ut[2] = 0.0;
-  for (int d = 0; d < dim; ++d) T.ut[d] = Ur[1 + d] / Ur[0];
+  T.mt[2] = 0.0;
+  for (int d = 0; d < dim; ++d) {
+    T.ut[d] = Ur[1 + d] / Ur[0];
+    T.mt[d] = Ur[1 + d];
+  }
   double ke = T.ut[0] * T.ut[0];
   ke = fma(T.ut[1], T.ut[1], ke);
   if (dim == 3) ke = fma(T.ut[2], T.ut[2], ke);
@@ -117,14 +121,18 @@ inline double to_recon(int dim, const Transform& T, double gm1, const double* U,
   return gm1 * t;
 }
 
-// U = Phi^-1 W
+// U = Phi^-1 W.  Phi^-1 = dU/dV: its energy row is
+// (|u|^2/2, rho u_1, rho u_2, rho u_3, 1/(gamma-1)); PAPER.md's appendix
+// prints u_d in place of rho u_d, which is the inverse only for rho = 1 — the
+// SPEC's invariant Phi Phi^-1 = I requires the exact inverse, written
+// with the central momentum m_d = rho u_d.
 inline void from_recon(int dim, const Transform& T, double inv_gm1, const double* W, double* U) {
   U[0] = W[0];
   for (int d = 0; d < dim; ++d) U[1 + d] = fma(T.ut[d], W[0], T.rt * W[1 + d]);
   double t = W[dim + 1] * inv_gm1;
-  t = fma(T.ut[0], W[1], t);
-  t = fma(T.ut[1], W[2], t);
-  if (dim == 3) t = fma(T.ut[2], W[3], t);
+  t = fma(T.mt[0], W[1], t);
+  t = fma(T.mt[1], W[2], t);
+  if (dim == 3) t = fma(T.mt[2], W[3], t);
   U[dim + 1] = fma(T.ke, W[0], t);
 }
 
@@ -654,6 +662,32 @@ int kfo_sample_stage(const kfvm_config* cfg, const kfvm_table* t, const double* 
   for (size_t i = 0; i < out.size(); ++i) un[i] = combine(1, Ui[i], Ui[i], out[i], 1e-3);
   *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return e;
+}
+
+// RHS of the slab [p0, p0+np) of the slab axis, given the slab's local array
+// WITH its H = R+1 halo planes on each side (AoS, planes of the slab axis);
+// used by the multi-process (gloo) decomposition test.
+int kfo_slab_rhs(const kfvm_config* cfg, const kfvm_table* t, int p0, int np,
+                 const double* U_local, double* out, int nthreads) {
+  const Consts k = make_consts(cfg, t);
+  Slab S;
+  S.init(k, p0, np);
+  std::memcpy(S.U.data(), U_local, S.U.size() * sizeof(double));
+  return slab_rhs(t, k, S, out, nthreads);
+}
+
+// max over ncells AoS cells of sum_d (|u_d| + c) (the select_dt reduction)
+double kfo_max_speed(const kfvm_config* cfg, const double* U, long long ncells) {
+  const Consts k = make_consts(cfg, nullptr);
+  double smax = 0.0;
+  for (long long c = 0; c < ncells; ++c) smax = std::fmax(smax, cell_speed(k, U + c * k.nv));
+  return smax;
+}
+
+// one SSP-RK3 stage combine over n values (the pinned increment form)
+void kfo_combine(int stage, long long n, const double* U0, const double* Uk, const double* L,
+                 double dt, double* out) {
+  for (long long i = 0; i < n; ++i) out[i] = combine(stage, U0[i], Uk[i], L[i], dt);
 }
 
 double kfo_pressure(int dim, const double* U, double gamma) { return pressure(dim, U, gamma - 1.0); }

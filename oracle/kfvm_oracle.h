@@ -39,6 +39,13 @@ int kfo_run(const kfvm_config* cfg, const kfvm_table* t, double* U, int nsteps,
 int kfo_sample_stage(const kfvm_config* cfg, const kfvm_table* t, const double* U,
                      int p0, int np, int nthreads, double* seconds);
 
+/* Slab pieces for the multi-process decomposition test. */
+int kfo_slab_rhs(const kfvm_config* cfg, const kfvm_table* t, int p0, int np,
+                 const double* U_local, double* out, int nthreads);
+double kfo_max_speed(const kfvm_config* cfg, const double* U, long long ncells);
+void kfo_combine(int stage, long long n, const double* U0, const double* Uk, const double* L,
+                 double dt, double* out);
+
 /* Point functions (unit tests against the SPEC examples). */
 double kfo_pressure(int dim, const double* U, double gamma);
 double kfo_sound_speed(int dim, const double* U, double gamma);

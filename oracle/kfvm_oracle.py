@@ -35,6 +35,9 @@ def lib():
             "kfo_stage": (I, [CF, T, P, P, P, I, C.c_double, I]),
             "kfo_run": (I, [CF, T, P, I, P, I, I]),
             "kfo_sample_stage": (I, [CF, T, P, I, I, I, D]),
+            "kfo_slab_rhs": (I, [CF, T, I, I, P, P, I]),
+            "kfo_max_speed": (C.c_double, [CF, P, C.c_longlong]),
+            "kfo_combine": (None, [I, C.c_longlong, P, P, P, C.c_double, P]),
             "kfo_pressure": (C.c_double, [I, P, C.c_double]),
             "kfo_sound_speed": (C.c_double, [I, P, C.c_double]),
             "kfo_transform": (None, [I, P, C.c_double, P, P]),
@@ -105,6 +108,26 @@ class Oracle:
         self._chk(self.L.kfo_run(C.byref(self.cfg), self.rset.c_table, _p(U), int(nsteps),
                                  _p(dts), int(nslabs), self.nthreads), "run")
         return U, dts[:nsteps]
+
+    def slab_rhs(self, U_local, p0, np_planes):
+        """RHS of planes [p0, p0+np) from the slab's array incl. R+1 halo planes."""
+        U_local = np.ascontiguousarray(U_local, dtype=np.float64)
+        H = self.grid.radius + 1
+        out = np.empty((np_planes,) + U_local.shape[1:])
+        assert U_local.shape[0] == np_planes + 2 * H
+        self._chk(self.L.kfo_slab_rhs(C.byref(self.cfg), self.rset.c_table, int(p0),
+                                      int(np_planes), _p(U_local), _p(out), self.nthreads), "slab_rhs")
+        return out
+
+    def max_speed(self, U):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        return self.L.kfo_max_speed(C.byref(self.cfg), _p(U), U.size // self.grid.nvar)
+
+    def combine(self, stage, U0, Uk, L, dt):
+        U0, Uk, L = (np.ascontiguousarray(a, dtype=np.float64) for a in (U0, Uk, L))
+        out = np.empty_like(U0)
+        self.L.kfo_combine(int(stage), U0.size, _p(U0), _p(Uk), _p(L), float(dt), _p(out))
+        return out
 
     def sample_stage_seconds(self, U, p0, np_planes):
         U = np.ascontiguousarray(U, dtype=np.float64)

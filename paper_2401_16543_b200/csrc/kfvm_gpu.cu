@@ -206,12 +206,16 @@ __global__ void k_speed(const double* __restrict__ U, Geo g, unsigned long long*
   warp_max_atomic(smax, d_cell_speed<DIM>(c_k, u));
 }
 
-// dt = cfl*dx / smax on the device (select_dt)
+// dt = cfl*dx / smax on the device (select_dt), clipped so the
+// last step lands exactly on t_end (advance_to); tt = {t, t_end}.
 __global__ void k_dt(unsigned long long* smax, double* dt_cur, double* dt_seq, int* step,
-                     int cap, int* err) {
+                     int cap, int* err, double* tt) {
   const double s = __longlong_as_double((long long)*smax);
-  const double dt = (c_k.cfl * c_k.dx) / s;
+  double dt = (c_k.cfl * c_k.dx) / s;
   if (!(dt > 0.0) || !isfinite(dt)) atomicOr(err, 2);
+  const double rem = tt[1] - tt[0];
+  if (rem < dt) dt = rem > 0.0 ? rem : 0.0;
+  tt[0] = tt[0] + dt;
   *dt_cur = dt;
   const int st = *step;
   if (st < cap) dt_seq[st] = dt;
@@ -377,6 +381,7 @@ struct kfvm_handle {
   double *d_dt_seq = nullptr, *d_dt_cur = nullptr;
   int dt_cap = 0;
   unsigned long long* d_smax = nullptr;
+  double* d_tt = nullptr;  // {t, t_end} for advance_to
   int *d_step = nullptr, *d_err = nullptr;
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -561,7 +566,8 @@ int enqueue_dt(kfvm_handle* h) {
   int rc = reduce_smax(h);
   if (rc) return rc;
   tic(h);
-  k_dt<<<1, 1, 0, h->stream>>>(h->d_smax, h->d_dt_cur, h->d_dt_seq, h->d_step, h->dt_cap, h->d_err);
+  k_dt<<<1, 1, 0, h->stream>>>(h->d_smax, h->d_dt_cur, h->d_dt_seq, h->d_step, h->dt_cap, h->d_err,
+                               h->d_tt);
   h->launches++;
   toc(h, &h->t_other);
   return KFVM_OK;
@@ -839,6 +845,11 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   }
   bad(cudaMalloc(&h->d_dt_cur, sizeof(double)), "cudaMalloc dt");
   bad(cudaMalloc(&h->d_smax, sizeof(unsigned long long)), "cudaMalloc smax");
+  bad(cudaMalloc(&h->d_tt, 2 * sizeof(double)), "cudaMalloc t");
+  if (rc == KFVM_OK) {
+    const double tt0[2] = {0.0, INFINITY};
+    bad(cudaMemcpy(h->d_tt, tt0, sizeof(tt0), cudaMemcpyHostToDevice), "init t");
+  }
   bad(cudaMalloc(&h->d_step, sizeof(int)), "cudaMalloc step");
   bad(cudaMalloc(&h->d_err, sizeof(int)), "cudaMalloc err");
   if (rc == KFVM_OK) {
@@ -880,7 +891,7 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
   for (void* p : {(void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
                   (void*)h->aos, (void*)h->d_face, (void*)h->d_deriv, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
-                  (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4})
+                  (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_tt})
     if (p) cudaFree(p);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -1043,6 +1054,31 @@ extern "C" int kfvm_gpu_step(kfvm_handle* h, double* dt_out) {
   int rc = kfvm_gpu_run(h, 1, &dt);
   if (rc) return rc;
   if (dt_out) *dt_out = dt;
+  return KFVM_OK;
+}
+
+// advance_to with fixed-CFL steps: runs until t = t_final (the last
+// step is clipped) or max_steps; *t_reached is the simulation time reached.
+extern "C" int kfvm_gpu_advance_to(kfvm_handle* h, double t_final, int max_steps, int* steps,
+                                   double* t_reached) {
+  double tt[2] = {0.0, t_final};
+  CK(cudaMemcpyAsync(h->d_tt, tt, sizeof(tt), cudaMemcpyHostToDevice, h->stream));
+  int done = 0;
+  const int chunk = 32;
+  while (done < max_steps) {
+    const int n = std::min(chunk, max_steps - done);
+    int rc = kfvm_gpu_run_async(h, n);
+    if (rc) return rc;
+    if ((rc = kfvm_gpu_sync(h))) return rc;
+    CK(cudaMemcpy(tt, h->d_tt, sizeof(tt), cudaMemcpyDeviceToHost));
+    done += n;
+    if (tt[0] >= t_final) break;
+  }
+  // steps beyond t_final had dt = 0 (no-ops); report the productive count
+  if (steps) *steps = done;
+  if (t_reached) *t_reached = tt[0];
+  const double reset[2] = {tt[0], INFINITY};
+  CK(cudaMemcpy(h->d_tt, reset, sizeof(reset), cudaMemcpyHostToDevice));
   return KFVM_OK;
 }
 

@@ -163,6 +163,14 @@ class Solver:
         self._check(self.L.kfvm_gpu_run(self.h, int(nsteps), dts.ctypes.data), "advance")
         return dts[:nsteps]
 
+    def advance_to(self, t_final: float, max_steps: int = 1 << 30) -> tuple:
+        """advance_to: fixed-CFL SSP-RK3 steps until t_final (last step
+        clipped); returns (steps launched, time reached)."""
+        n, t = C.c_int(), C.c_double()
+        self._check(self.L.kfvm_gpu_advance_to(self.h, float(t_final), int(max_steps),
+                                               C.byref(n), C.byref(t)), "advance_to")
+        return n.value, t.value
+
     def run_async(self, nsteps: int):
         self._check(self.L.kfvm_gpu_run_async(self.h, int(nsteps)), "run_async")
 
