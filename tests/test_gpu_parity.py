@@ -126,3 +126,64 @@ def test_runtime_error_on_inadmissible_state(require_gpu):
         s.set_state(U)
         with pytest.raises(K.KfvmRuntimeError):
             s.advance(1)
+
+
+@pytest.mark.parametrize("idx,n", [(1, 20), (2, 24), (3, 10), (4, 10)])
+def test_engines_bitwise_identical(require_gpu, idx, n):
+    """generic / unrolled-DFMA / DMMA reconstruction engines agree bit for bit."""
+    g, ic, U, rset = _setup(idx, n, {})
+    outs = []
+    for eng in (0, 1, 2):
+        with K.Solver(g, rset) as s:
+            s.set_option("engine", eng)
+            s.set_state(U)
+            d = s.advance(2)
+            outs.append((d, s.get_state()))
+    for d, A in outs[1:]:
+        assert np.array_equal(d, outs[0][0]) and np.array_equal(A, outs[0][1])
+
+
+def test_advance_to_matches_oracle(require_gpu):
+    """advance_to: fixed-CFL steps, last one clipped onto t_final."""
+    from paper_2401_16543_b200.config import GridConfig
+    g = GridConfig(dim=2, radius=2, nx=24, ny=24, bc="periodic", dx=20.0 / 24, cfl=0.4)
+    ic = ICSpec("vortex", origin=(-10.0, -10.0, 0.0))
+    U0 = K.initial_condition(g, ic)
+    rset = K.precompute(2, dim=2)
+    o = Oracle(g, rset)
+    U, t, n = U0.copy(), 0.0, 0
+    while t < 1.0:
+        dt = min(o.select_dt(U), 1.0 - t)
+        U1 = o.stage(U, U, 1, dt)
+        U2 = o.stage(U, U1, 2, dt)
+        U = o.stage(U, U2, 3, dt)
+        t += dt
+        n += 1
+    with K.Solver(g, rset) as s:
+        s.set_state(U0)
+        steps, tg = s.advance_to(1.0)
+        Ug = s.get_state()
+    assert tg == t and steps >= n
+    assert np.array_equal(Ug, U)
+
+
+def test_isentropic_vortex_eoc_gpu(require_gpu):
+    """S:791 acceptance / PAPER Table 1 on the GPU: R=2 64^2 -> 128^2 EOC >= 3.5
+    (paper 3.95); R=3 32^2 -> 64^2 EOC >= 3.0 (paper 3.32)."""
+    import math
+    from paper_2401_16543_b200.config import GridConfig
+    ic = ICSpec("vortex", origin=(-10.0, -10.0, 0.0))
+
+    def l1(n, R):
+        g = GridConfig(dim=2, radius=R, nx=n, ny=n, bc="periodic", dx=20.0 / n, cfl=0.4)
+        U0 = K.initial_condition(g, ic)
+        with K.Solver(g) as s:
+            s.set_state(U0)
+            s.advance_to(20.0)
+            U = s.get_state()
+        return np.abs(U[..., 0] - U0[..., 0]).sum() * g.dx ** 2
+
+    e = {n: l1(n, 2) for n in (64, 128)}
+    assert math.log(e[64] / e[128]) / math.log(2) >= 3.5, e
+    e3 = {n: l1(n, 3) for n in (32, 64)}
+    assert math.log(e3[32] / e3[64]) / math.log(2) >= 3.0, e3
