@@ -10,7 +10,8 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 CXXFLAGS := -std=gnu++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra
 MINB ?= 2
 MMAMINB ?= 3
-NVFLAGS := $(ARCH) -DKFVM_FAST_MINB=$(MINB) -DKFVM_MMA_MINB=$(MMAMINB) -std=c++17 -O3 -lineinfo -fmad=false -Xcompiler -fPIC,-ffp-contract=off \
+EXTRA ?=
+NVFLAGS := $(ARCH) $(EXTRA) -DKFVM_FAST_MINB=$(MINB) -DKFVM_MMA_MINB=$(MMAMINB) -std=c++17 -O3 -lineinfo -fmad=false -Xcompiler -fPIC,-ffp-contract=off \
            -Xptxas -v --expt-relaxed-constexpr
 
 PKG := paper_2401_16543_b200

@@ -209,6 +209,10 @@ int kfvm_gpu_last_error(kfvm_handle* h, char* buf, size_t n);
  * kfvm_ic_generate (the per-point arithmetic is IEEE add/mul/div only). */
 int kfvm_gpu_ic_generate(kfvm_handle* h, const kfvm_ic_params* ic);
 
+/* Diagnostics: per-phase cycle counters of the reconstruction kernels
+ * (non-zero only in a -DKFVM_PHASE_TIMING build). */
+int kfvm_phase_cycles(unsigned long long* out8, int reset);
+
 /* FP64 roofline denominators measured on the current device: DFMA pipe
  * (8 independent chains per thread) and DMMA (mma.sync m8n8k4.f64). */
 int kfvm_fp64_peak(double* dfma_tflops, double* dmma_tflops, double* sm_clock_ghz);

@@ -180,6 +180,69 @@ void weno_field(const kfvm_table* t, const Consts& k, const double* g, double* b
   }
 }
 
+// WENO-AO of one cell for all variables, in "U-space" form:
+// every derivative / face-point vector is contracted with the RAW conserved
+// variables of the stencil (stencil-order fma chains), and the linear map
+// Phi (constant part dropped) is applied to each vector of nv
+// contractions.  Mathematically identical to reconstructing W = Phi U cell by
+// cell; this is the pinned order the GPU tensor-core path reproduces.
+void weno_cell_u(const kfvm_table* t, const Consts& k, const Transform& T,
+                 const double* const* cells, double* W /* [np][nv] */,
+                 double* beta_out /* [NS][nv] or null */) {
+  const int NS = t->n_stencils, nv = k.nv, dim = k.dim;
+  double c[KFVM_MAX_STENCILS][5];
+  double wt[KFVM_MAX_STENCILS][5];
+  for (int q = 0; q < NS; ++q) {
+    const int N = t->size[q];
+    const int* gat = t->gather + t->cell_offset[q];
+    const double* Dq = t->deriv + (size_t)t->cell_offset[q] * t->n_alpha;
+    double beta[5] = {0, 0, 0, 0, 0};
+    for (int a = 0; a < t->n_alpha; ++a) {
+      double D[5];
+      for (int u = 0; u < nv; ++u) {
+        double acc = 0.0;
+        for (int h = 0; h < N; ++h) acc = fma(Dq[a * N + h], cells[gat[h]][u], acc);
+        D[u] = acc;
+      }
+      for (int v = 0; v < nv; ++v) {
+        const double dv = to_recon(dim, T, k.gm1, D, v);
+        beta[v] = fma(k.scale[a], dv * dv, beta[v]);
+      }
+    }
+    for (int v = 0; v < nv; ++v) {
+      if (beta_out) beta_out[q * nv + v] = beta[v];
+      wt[q][v] = t->gamma_lin[q] * (1.0 / fma(beta[v], beta[v], k.eps));
+    }
+  }
+  const double inv_g0 = 1.0 / t->gamma_lin[0];
+  for (int v = 0; v < nv; ++v) {
+    double sum = wt[0][v];
+    for (int q = 1; q < NS; ++q) sum = sum + wt[q][v];
+    const double inv_sum = 1.0 / sum;
+    c[0][v] = (wt[0][v] * inv_sum) * inv_g0;
+    for (int q = 1; q < NS; ++q) c[q][v] = fma(-c[0][v], t->gamma_lin[q], wt[q][v] * inv_sum);
+  }
+  for (int s = 0; s < t->n_points; ++s) {
+    double val[5] = {0, 0, 0, 0, 0};
+    for (int q = 0; q < NS; ++q) {
+      const int N = t->size[q];
+      const int* gat = t->gather + t->cell_offset[q];
+      const double* r = t->face + (size_t)t->cell_offset[q] * t->n_points + (size_t)s * N;
+      double P[5];
+      for (int u = 0; u < nv; ++u) {
+        double acc = 0.0;
+        for (int h = 0; h < N; ++h) acc = fma(r[h], cells[gat[h]][u], acc);
+        P[u] = acc;
+      }
+      for (int v = 0; v < nv; ++v) {
+        const double w = to_recon(dim, T, k.gm1, P, v);
+        val[v] = (q == 0) ? c[0][v] * w : fma(c[q][v], w, val[v]);
+      }
+    }
+    for (int v = 0; v < nv; ++v) W[s * nv + v] = val[v];
+  }
+}
+
 // ------------------------------------------------------- positivity limiter
 // nbr: 3^dim averages (i fastest), centre at index (3^dim)/2.  Returns 0 ok,
 // 2 if the cell average itself is inadmissible.
@@ -269,73 +332,69 @@ inline void exact_flux(int dim, int d, const double* U, double un, double p, dou
   F[nv - 1] = (U[nv - 1] + p) * un;
 }
 
-struct Speeds {
-  double sl, sr;
-};
-
-inline Speeds batten(int dim, double gamma, double gm1, int d, const double* UL, const double* UR,
-                     double pL, double pR, double* uL, double* uR) {
-  const int nv = dim + 2;
-  const double cL = sound(gamma, pL, UL[0]), cR = sound(gamma, pR, UR[0]);
-  const double HL = (UL[nv - 1] + pL) / UL[0], HR = (UR[nv - 1] + pR) / UR[0];
-  const double sl = std::sqrt(UL[0]), sr = std::sqrt(UR[0]);
-  const double den = sl + sr;
-  double roe[3] = {0, 0, 0};
-  for (int m = 0; m < dim; ++m) roe[m] = fma(sl, uL[m], sr * uR[m]) / den;
-  const double Hroe = fma(sl, HL, sr * HR) / den;
-  double q2 = roe[0] * roe[0];
-  q2 = fma(roe[1], roe[1], q2);
-  if (dim == 3) q2 = fma(roe[2], roe[2], q2);
-  const double c2 = gm1 * (Hroe - 0.5 * q2);
-  const double croe = std::sqrt(std::fmax(c2, 0.0));
-  Speeds s;
-  s.sl = std::fmin(uL[d] - cL, roe[d] - croe);
-  s.sr = std::fmax(uR[d] + cR, roe[d] + croe);
-  return s;
-}
-
+// Batten/Roe speeds + HLL/HLLC.  Pinned form: one reciprocal
+// per side (1/rho) and per Roe denominator, so a solve costs 6 IEEE
+// divisions (HLLC; 4 for HLL) instead of ~16.
 void riemann(const Consts& k, int d, const double* UL, const double* UR, double* F,
              double* speeds = nullptr) {
   const int dim = k.dim, nv = k.nv;
+  const double irL = 1.0 / UL[0], irR = 1.0 / UR[0];
   double uL[3] = {0, 0, 0}, uR[3] = {0, 0, 0};
   for (int m = 0; m < dim; ++m) {
-    uL[m] = UL[1 + m] / UL[0];
-    uR[m] = UR[1 + m] / UR[0];
+    uL[m] = UL[1 + m] * irL;
+    uR[m] = UR[1 + m] * irR;
   }
-  const double pL = pressure(dim, UL, k.gm1), pR = pressure(dim, UR, k.gm1);
-  const Speeds S = batten(dim, k.gamma, k.gm1, d, UL, UR, pL, pR, uL, uR);
+  double qL = UL[1] * UL[1], qR = UR[1] * UR[1];
+  qL = fma(UL[2], UL[2], qL);
+  qR = fma(UR[2], UR[2], qR);
+  if (dim == 3) {
+    qL = fma(UL[3], UL[3], qL);
+    qR = fma(UR[3], UR[3], qR);
+  }
+  const double pL = k.gm1 * (UL[nv - 1] - 0.5 * (qL * irL));
+  const double pR = k.gm1 * (UR[nv - 1] - 0.5 * (qR * irR));
+  const double cL = std::sqrt((k.gamma * pL) * irL), cR = std::sqrt((k.gamma * pR) * irR);
+  const double HL = (UL[nv - 1] + pL) * irL, HR = (UR[nv - 1] + pR) * irR;
+  const double sl = std::sqrt(UL[0]), sr = std::sqrt(UR[0]);
+  const double iden = 1.0 / (sl + sr);
+  double roe[3] = {0, 0, 0};
+  for (int m = 0; m < dim; ++m) roe[m] = fma(sl, uL[m], sr * uR[m]) * iden;
+  const double Hroe = fma(sl, HL, sr * HR) * iden;
+  double q2 = roe[0] * roe[0];
+  q2 = fma(roe[1], roe[1], q2);
+  if (dim == 3) q2 = fma(roe[2], roe[2], q2);
+  const double croe = std::sqrt(std::fmax(k.gm1 * (Hroe - 0.5 * q2), 0.0));
+  const double SL = std::fmin(uL[d] - cL, roe[d] - croe);
+  const double SR = std::fmax(uR[d] + cR, roe[d] + croe);
   double FL[5], FR[5];
   exact_flux(dim, d, UL, uL[d], pL, FL);
   exact_flux(dim, d, UR, uR[d], pR, FR);
-  const double aL = UL[0] * (S.sl - uL[d]);
-  const double aR = UR[0] * (S.sr - uR[d]);
-  double sstar = 0.0;
-  {
-    double num = fma(aL, uL[d], pR - pL);
-    num = fma(-aR, uR[d], num);
-    sstar = num / (aL - aR);
-  }
+  const double aL = UL[0] * (SL - uL[d]);
+  const double aR = UR[0] * (SR - uR[d]);
+  double num = fma(aL, uL[d], pR - pL);
+  num = fma(-aR, uR[d], num);
+  const double sstar = num / (aL - aR);
   if (speeds) {
-    speeds[0] = S.sl;
-    speeds[1] = S.sr;
+    speeds[0] = SL;
+    speeds[1] = SR;
     speeds[2] = sstar;
   }
-  if (S.sl >= 0.0) {
+  if (SL >= 0.0) {
     for (int v = 0; v < nv; ++v) F[v] = FL[v];
     return;
   }
-  if (S.sr <= 0.0) {
+  if (SR <= 0.0) {
     for (int v = 0; v < nv; ++v) F[v] = FR[v];
     return;
   }
   if (k.riemann == KFVM_RIEMANN_HLL) {
-    const double ssr = S.sl * S.sr;
-    const double den = S.sr - S.sl;
+    const double ssr = SL * SR;
+    const double iw = 1.0 / (SR - SL);
     for (int v = 0; v < nv; ++v) {
-      double t = S.sr * FL[v];
-      t = fma(-S.sl, FR[v], t);
+      double t = SR * FL[v];
+      t = fma(-SL, FR[v], t);
       t = fma(ssr, UR[v] - UL[v], t);
-      F[v] = t / den;
+      F[v] = t * iw;
     }
     return;
   }
@@ -344,14 +403,15 @@ void riemann(const Consts& k, int d, const double* UL, const double* UR, double*
   const double* UK = left ? UL : UR;
   const double* FK = left ? FL : FR;
   const double* uK = left ? uL : uR;
-  const double SK = left ? S.sl : S.sr;
+  const double SK = left ? SL : SR;
   const double aK = left ? aL : aR;
   const double pK = left ? pL : pR;
+  const double irK = left ? irL : irR;
   const double fac = aK / (SK - sstar);
   double Us[5];
   Us[0] = fac;
   for (int m = 0; m < dim; ++m) Us[1 + m] = fac * (m == d ? sstar : uK[m]);
-  const double e = fma(sstar - uK[d], sstar + pK / aK, UK[nv - 1] / UK[0]);
+  const double e = fma(sstar - uK[d], sstar + pK / aK, UK[nv - 1] * irK);
   Us[nv - 1] = fac * e;
   for (int v = 0; v < nv; ++v) F[v] = fma(SK, Us[v] - UK[v], FK[v]);
 }
@@ -434,13 +494,8 @@ int cell_states(const kfvm_table* t, const Consts& k, const Slab& S, int i, int 
   std::vector<const double*> cells(N0);
   for (int h = 0; h < N0; ++h)
     cells[h] = S.at(i + t->offsets[3 * h], j + t->offsets[3 * h + 1], kk + t->offsets[3 * h + 2]);
-  double g[128], vals[64];
   double W[64 * 5];
-  for (int v = 0; v < nv; ++v) {
-    for (int h = 0; h < N0; ++h) g[h] = to_recon(dim, T, k.gm1, cells[h], v);
-    weno_field(t, k, g, nullptr, nullptr, vals);
-    for (int s = 0; s < np; ++s) W[s * nv + v] = vals[s];
-  }
+  weno_cell_u(t, k, T, cells.data(), W, nullptr);
   for (int s = 0; s < np; ++s) from_recon(dim, T, k.inv_gm1, W + s * nv, st + s * nv);
   double nbr[27 * 5];
   const int kr = dim == 3 ? 1 : 0;

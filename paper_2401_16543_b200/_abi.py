@@ -88,6 +88,7 @@ EXPORTS = [
     ("kfvm_gpu_last_error", C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
     ("kfvm_gpu_ic_generate", C.c_int, [C.c_void_p, C.POINTER(KfvmIcParams)]),
     ("kfvm_fp64_peak", C.c_int, [C.POINTER(C.c_double)] * 3),
+    ("kfvm_phase_cycles", C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
     ("kfvm_gpu_advance_to", C.c_int, [C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_int),
                                       C.POINTER(C.c_double)]),
 ]

@@ -55,8 +55,14 @@ struct Chunk {
 
 __device__ __forceinline__ int remap(int i, int n, int bc) {
   if (bc == KFVM_BC_PERIODIC) {
-    i %= n;
-    return i < 0 ? i + n : i;
+    // stencil offsets are at most R+1 cells beyond an edge: one conditional
+    // wrap covers every grid with n >= R+1; the modulo is the rare fallback
+    i = i < 0 ? i + n : (i >= n ? i - n : i);
+    if ((unsigned)i >= (unsigned)n) {
+      i %= n;
+      i = i < 0 ? i + n : i;
+    }
+    return i;
   }
   return i < 0 ? 0 : (i >= n ? n - 1 : i);
 }
@@ -74,6 +80,7 @@ constexpr int full_size(int dim, int R) {
 constexpr int npoints(int dim, int R) { return dim == 2 ? 4 * R : 6 * R * R; }
 
 #include "kfvm_recon.cuh"
+#include "kfvm_recon_u.cuh"
 
 // ------------------------------------------------------------------ k_flux
 template <int DIM>
@@ -387,7 +394,8 @@ struct kfvm_handle {
   cudaGraphExec_t graph = nullptr;
   bool timing = false;
   bool fast = true;
-  int engine = 2;  // 0 generic, 1 DFMA unrolled (k_states_fast), 2 DMMA (k_states_mma)
+  int engine = 2;  // 0 generic (k_states), 2 tensor-core U-space (k_states_u)
+  int kz = 16;     // planes marched by one k_states_u CTA
   double *d_Bd = nullptr, *d_Bf = nullptr;
   int* d_gat4 = nullptr;
   cudaEvent_t ev[2];
@@ -444,14 +452,12 @@ void toc(kfvm_handle* h, double* acc) {
 template <int DIM, int R>
 void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   tic(h);
-  const long long nblk = (long long)((ch.ex + 31) / 32) * ch.em * ch.ep;
   if constexpr (!(DIM == 3 && R == 3)) {
     if (h->engine == 2) {
-      k_states_mma<DIM, R><<<(unsigned)nblk, 32 * (DIM + 2), MmaCfg<DIM, R>::bytes(), h->stream>>>(
-          U, h->Pr, h->St, h->g, ch, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4);
-    } else if (h->engine == 1) {
-      k_states_fast<DIM, R><<<(unsigned)nblk, 32 * (DIM + 2), 0, h->stream>>>(U, h->Pr, h->St, h->g,
-                                                                            ch, h->d_err);
+      const int KZ = h->kz;
+      const long long nblk2 = (long long)((ch.ex + 31) / 32) * ch.em * ((ch.ep + KZ - 1) / KZ);
+      k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
+          U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4);
     } else {
       k_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
                                                                     h->d_err);
@@ -641,12 +647,10 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   for (int i = 0; i < G::NTOT; ++i)
     if (t->gather[i] != G::GATHER[i])
       return fail(h, KFVM_ERR_CONFIG, "table substencils differ from kfvm_gen.cuh");
-  CK(cudaMemcpyToSymbol(G::face_symbol(), t->face, sizeof(double) * G::NTOT * G::NP));
-  CK(cudaMemcpyToSymbol(G::deriv_symbol(), t->deriv, sizeof(double) * G::NTOT * G::NA));
   // DMMA operands: per 4-entry chunk of each stencil (zero-padded at the
   // front), B fragments in lane order (k = lane%4, column = lane/4) and the
   // S0 position of every chunk slot
-  using M = MmaCfg<D, R>;
+  using M = UCfg<D, R>;
   std::vector<double> bd((size_t)G::NCHUNK * M::ND * 32, 0.0), bf((size_t)G::NCHUNK * M::NPT * 32, 0.0);
   std::vector<int> g4((size_t)G::NCHUNK * 5, 0);  // gather rows, then sQ (stencil | last<<8)
   for (int q = 0, ck = 0; q < G::NS; ++q) {
@@ -679,7 +683,7 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   CK(cudaMemcpy(h->d_Bd, bd.data(), bd.size() * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_Bf, bf.data(), bf.size() * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_gat4, g4.data(), g4.size() * sizeof(int), cudaMemcpyHostToDevice));
-  CK(cudaFuncSetAttribute(k_states_mma<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(k_states_u<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)M::bytes()));
   return KFVM_OK;
 }
@@ -713,7 +717,8 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   h->R = cfg->radius;
   h->nv = cfg->dim + 2;
   h->NP = t->n_points;
-  h->engine = cfg->dim == 3 ? 2 : 1;  // DMMA for 3-D, unrolled DFMA for 2-D (measured)
+  h->engine = 2;
+  h->kz = 16;
   if (dist) {
     h->rank = dist->rank;
     h->nranks = dist->nranks;
@@ -1082,6 +1087,23 @@ extern "C" int kfvm_gpu_advance_to(kfvm_handle* h, double t_final, int max_steps
   return KFVM_OK;
 }
 
+// Per-phase cycle counters of the reconstruction kernels (built with
+// -DKFVM_PHASE_TIMING; zeros otherwise).  reset != 0 clears them.
+extern "C" int kfvm_phase_cycles(unsigned long long* out8, int reset) {
+#ifdef KFVM_PHASE_TIMING
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, g_phase_cycles, 8 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+#else
+  for (int i = 0; i < 8; ++i) out8[i] = 0;
+  (void)reset;
+#endif
+  return KFVM_OK;
+}
+
 extern "C" void* kfvm_gpu_stream(kfvm_handle* h) { return (void*)h->stream; }
 extern "C" long long kfvm_gpu_launch_count(kfvm_handle* h) { return h->launches; }
 
@@ -1089,11 +1111,20 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
   std::string n(name ? name : "");
   if (n == "fast_states" || n == "engine") {
     if (n == "engine") {
-      if (value < 0 || value > 2) return fail(h, KFVM_ERR_CONFIG, "engine must be 0, 1 or 2");
+      if (value != 0 && value != 2) return fail(h, KFVM_ERR_CONFIG, "engine must be 0 or 2");
       h->engine = (int)value;
     } else {
       h->engine = value ? 2 : 0;
     }
+    if (h->graph) {
+      cudaGraphExecDestroy(h->graph);
+      h->graph = nullptr;
+    }
+    return KFVM_OK;
+  }
+  if (n == "kz") {
+    if (value < 1) return fail(h, KFVM_ERR_CONFIG, "kz must be >= 1");
+    h->kz = (int)value;
     if (h->graph) {
       cudaGraphExecDestroy(h->graph);
       h->graph = nullptr;

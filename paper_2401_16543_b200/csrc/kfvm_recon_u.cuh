@@ -1,0 +1,462 @@
+// kfvm_recon_u.cuh — reconstruct_states on the FP64 tensor cores,
+// "U-space" form, plane-marching CTAs with a cp.async ring buffer.
+// Included inside namespace kfvm_b200 by kfvm_gpu.cu.
+//
+// Contract (oracle weno_cell_u): every derivative / face-point
+// vector of every (sub)stencil is contracted with the RAW conserved
+// variables (stencil-order fma chains, here as zero-padded 4-entry DMMA
+// chunks: mma.sync.m8n8k4.f64 == the sequential fma chain, measured), then
+// the linear map Phi is applied to the vector of nv contractions.
+//
+// Work decomposition.  CTA = 4 warps = a 32-cell x-segment of one row; it
+// marches along the slab axis over KZ extended planes.  Warp w owns cells
+// w, w+4, .., w+28 of the segment and ALL variables: the DMMA A operand (8 cells x 4
+// stencil entries) is read straight from the staged U region, B (4 entries
+// x 8 columns) is the weight table in fragment order.  The accumulator layout
+// puts all nv variables of one (cell, column) in one thread, so Phi, the
+// WENO-AO combination, Phi^-1 and the positivity limiter run in registers;
+// the 4 lanes of a quad share a cell and reduce with shuffles.
+#ifndef KFVM_RECON_U_CUH_
+#define KFVM_RECON_U_CUH_
+
+#include <cuda_pipeline.h>
+
+#ifndef KFVM_U_MINB
+#define KFVM_U_MINB 2
+#endif
+
+template <int D, int R>
+struct UCfg {
+  using G = Gen<D, R>;
+  static constexpr int nv = D + 2;
+  static constexpr int ND = (G::NA + 7) / 8;
+  static constexpr int NPT = (G::NP + 7) / 8;
+  static constexpr int RX = 32 + 2 * R;                 // region x extent
+  static constexpr int RY = D == 3 ? 2 * R + 1 : 1;     // region mid extent
+  static constexpr int RROW = RY * RX;                  // one variable of a plane
+  static constexpr int PL = nv * RROW;                  // one region plane
+  static constexpr int RING = 2 * R + 2;                // planes in the ring
+  static constexpr int NX = 34, NY = D == 3 ? 3 : 1;    // prims neighbourhood
+  static constexpr int NF = 3 + D;                      // p, c, 1/rho, u_d
+  static constexpr int PROW = NY * NX;
+  static constexpr int PPL = NF * PROW;
+  static constexpr int PRING = 4;
+  static constexpr int SCW = G::NS * nv * 8;            // beta / c_q per warp
+  static constexpr int SB = G::NCHUNK * (ND + NPT) * 32;  // B fragments
+  static constexpr size_t bytes() {
+    return sizeof(double) * (RING * PL + PRING * PPL + 4 * SCW + SB) +
+           sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK);
+  }
+};
+
+template <int D>
+__device__ __forceinline__ double phi_row(const DTransform& T, const double* X, int v) {
+  // W_v = (Phi X)_v, constant part dropped (same formula as d_to_recon)
+  if (v == 0) return X[0];
+  if (v <= D) return fma(-T.ut[v - 1], X[0], X[v]) * T.inv_r;
+  double t = fma(T.ke, X[0], X[D + 1]);
+  t = fma(-T.ut[0], X[1], t);
+  t = fma(-T.ut[1], X[2], t);
+  if (D == 3) t = fma(-T.ut[2], X[3], t);
+  return c_k.gm1 * t;
+}
+
+template <int D, int R>
+__global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
+    k_states_u(const double* __restrict__ U, const double* __restrict__ Pr,
+               double* __restrict__ St, Geo g, Chunk ch, int KZ, int* __restrict__ err,
+               const double* __restrict__ Bd, const double* __restrict__ Bf,
+               const int* __restrict__ gat4) {
+  using G = Gen<D, R>;
+  using C = UCfg<D, R>;
+  constexpr int nv = C::nv, NP = G::NP, NS = G::NS, ND = C::ND, NPT = C::NPT;
+  extern __shared__ double smem[];
+  double* sRing = smem;                          // [RING][nv][RY][RX]
+  double* sPr = sRing + C::RING * C::PL;         // [PRING][NF][NY][NX]
+  double* sC = sPr + C::PRING * C::PPL;          // [warp][q][v][8]
+  double* sBd = sC + 4 * C::SCW;                 // B fragments [chunk][n][lane]
+  double* sBf = sBd + G::NCHUNK * ND * 32;
+  int* sTab = reinterpret_cast<int*>(sBf + G::NCHUNK * NPT * 32);  // [chunk][4] {inplane, oz}
+  int* sQ = sTab + 8 * G::NCHUNK;                        // stencil | last << 8
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int k4 = lane & 3, r8 = lane >> 2;
+  // chunk tables: region offsets of every chunk slot
+  for (int i = threadIdx.x; i < 4 * G::NCHUNK; i += 128) {
+    const int h = gat4[i];
+    const int ox = G::off(h, 0);
+    const int oy = D == 3 ? G::off(h, 1) : 0;
+    const int oz = D == 3 ? G::off(h, 2) : G::off(h, 1);
+    sTab[2 * i] = (oy + (D == 3 ? R : 0)) * C::RX + ox + R;
+    sTab[2 * i + 1] = oz;
+  }
+  for (int i = threadIdx.x; i < G::NCHUNK; i += 128) sQ[i] = gat4[4 * G::NCHUNK + i];
+  for (int i = threadIdx.x; i < G::NCHUNK * ND * 32; i += 128) sBd[i] = __ldg(Bd + i);
+  for (int i = threadIdx.x; i < G::NCHUNK * NPT * 32; i += 128) sBf[i] = __ldg(Bf + i);
+
+  const int nseg = (ch.ex + 31) >> 5;
+  int bid = blockIdx.x;
+  const int seg = bid % nseg;
+  bid /= nseg;
+  const int b = bid % ch.em;          // extended mid index
+  const int zblk = bid / ch.em;
+  const int cstart = zblk * KZ, cend = min(ch.ep, cstart + KZ);
+  const int j = D == 3 ? b - 1 : 0;
+  const int x0 = seg * 32 - 1;        // x of the segment's first cell
+  // warp w owns the cells w, w+4, ..., w+28 of the segment (stride 4): the 4
+  // slots of a DMMA chunk are mostly consecutive x offsets, and with stride-4
+  // rows the 16 (cell, slot) words of a half-warp fall in distinct banks
+  const int cidx = w + 4 * r8;
+  const int a = seg * 32 + cidx;  // extended x index of this lane's cell
+  const bool active = a < ch.ex;
+  const int xr = cidx + R;            // the cell's x in the region
+
+  // x indices (remapped) of the region columns this thread copies
+  auto load_plane = [&](int p) {  // region plane p -> ring slot
+    double* dst = sRing + ((p + 4 * C::RING) % C::RING) * C::PL;
+    const long long pbase = (long long)(p + g.H) * g.pstride;
+    for (int i = threadIdx.x; i < C::PL; i += 128) {
+      const int rx = i % C::RX, rr = i / C::RX;
+      const int ry = rr % C::RY, v = rr / C::RY;
+      const int xx = remap(x0 - R + rx, g.nx, c_k.bc);
+      const long long off = v * g.vstride + pbase + xx +
+                            (D == 3 ? (long long)remap(j - R + ry, g.nm, c_k.bc) * g.nx : 0);
+      __pipeline_memcpy_async(dst + i, U + off, sizeof(double));
+    }
+  };
+  auto load_prims = [&](int p) {  // prims plane p -> prims ring slot
+    double* dst = sPr + ((p + 4 * C::PRING) % C::PRING) * C::PPL;
+    const long long pbase = (long long)(p + g.H) * g.pstride;
+    for (int i = threadIdx.x; i < C::PPL; i += 128) {
+      const int rx = i % C::NX, rr = i / C::NX;
+      const int ry = rr % C::NY, f = rr / C::NY;
+      const int xx = remap(x0 - 1 + rx, g.nx, c_k.bc);
+      const long long off = f * g.vstride + pbase + xx +
+                            (D == 3 ? (long long)remap(j - 1 + ry, g.nm, c_k.bc) * g.nx : 0);
+      __pipeline_memcpy_async(dst + i, Pr + off, sizeof(double));
+    }
+  };
+  {
+    const int p = ch.c0 - 1 + cstart;
+    for (int oz = -R; oz <= R; ++oz) load_plane(p + oz);
+    for (int oz = -1; oz <= 1; ++oz) load_prims(p + oz);
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
+  }
+  __syncthreads();
+
+  double* sCw = sC + w * C::SCW;
+  PHASE_T0();
+  for (int c = cstart; c < cend; ++c) {
+    const int p = ch.c0 - 1 + c;
+    if (c + 1 < cend) {
+      load_plane(p + R + 1);
+      load_prims(p + 2);
+    }
+    __pipeline_commit();
+    // ring slot of plane p + oz (oz in [-R, R]) without a local pointer array
+    const int slot0 = (p - R + 4 * C::RING) % C::RING;  // slot of plane p - R
+    auto plane = [&](int ozr) -> const double* {       // ozr = oz + R
+      const int sl = slot0 + ozr;
+      return sRing + (sl >= C::RING ? sl - C::RING : sl) * C::PL;
+    };
+    const double* pr0 = sPr + ((p + 4 * C::PRING) % C::PRING) * C::PPL;
+    const double* prm = sPr + ((p - 1 + 4 * C::PRING) % C::PRING) * C::PPL;
+    const double* prp = sPr + ((p + 1 + 4 * C::PRING) % C::PRING) * C::PPL;
+    const int icn = (D == 3 ? C::NX : 0) + xr - R + 1;  // cell centre in a prims plane
+    const int icr = (D == 3 ? R * C::RX : 0) + xr;      // cell centre in a region plane
+    // ---- transform of the cell average (identical to d_make_transform)
+    DTransform T;
+    T.rt = plane(R)[icr];
+    T.inv_r = pr0[2 * C::PROW + icn];
+    T.ut[2] = T.mt[2] = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      T.ut[d] = pr0[(3 + d) * C::PROW + icn];
+      T.mt[d] = plane(R)[(1 + d) * C::RROW + icr];
+    }
+    {
+      double ke = T.ut[0] * T.ut[0];
+      ke = fma(T.ut[1], T.ut[1], ke);
+      if (D == 3) ke = fma(T.ut[2], T.ut[2], ke);
+      T.ke = 0.5 * ke;
+    }
+    PHASE_MARK(0);
+    // ---- pass 1: derivative columns -> beta_{q,v}
+    {
+      double acc[nv][ND][2];
+#pragma unroll
+      for (int u = 0; u < nv; ++u)
+#pragma unroll
+        for (int n = 0; n < ND; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+      int q = 0;
+      // software pipeline: fragments of chunk ck+1 load while chunk ck issues
+      double av[nv], bv[ND];
+      {
+        const int inpl = sTab[2 * k4], oz = sTab[2 * k4 + 1];
+        const double* ap = plane(oz + R) + inpl + cidx;
+#pragma unroll
+        for (int u = 0; u < nv; ++u) av[u] = ap[u * C::RROW];
+#pragma unroll
+        for (int n = 0; n < ND; ++n) bv[n] = sBd[n * 32 + lane];
+      }
+#pragma unroll 1
+      for (int ck = 0; ck < G::NCHUNK; ++ck) {
+        const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
+        const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
+        const double* ap = plane(oz + R) + inpl + cidx;
+        double an[nv], bn[ND];
+#pragma unroll
+        for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
+#pragma unroll
+        for (int n = 0; n < ND; ++n) bn[n] = sBd[(cn * ND + n) * 32 + lane];
+#pragma unroll
+        for (int n = 0; n < ND; ++n)
+#pragma unroll
+          for (int u = 0; u < nv; ++u) dmma(acc[u][n][0], acc[u][n][1], av[u], bv[n]);
+#pragma unroll
+        for (int u = 0; u < nv; ++u) av[u] = an[u];
+#pragma unroll
+        for (int n = 0; n < ND; ++n) bv[n] = bn[n];
+        if (sQ[ck] & 256) {
+          // acc[u][n][e]: cell r8, alpha = 8n + 2k4 + e; Phi per (alpha), then
+          // beta_v = sequential chain over alpha (quad shuffles)
+          double dv[nv][ND][2];
+#pragma unroll
+          for (int n = 0; n < ND; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              double X[nv];
+#pragma unroll
+              for (int u = 0; u < nv; ++u) X[u] = acc[u][n][e];
+#pragma unroll
+              for (int v = 0; v < nv; ++v) dv[v][n][e] = phi_row<D>(T, X, v);
+            }
+          double bq[nv];
+#pragma unroll
+          for (int v = 0; v < nv; ++v) bq[v] = 0.0;
+#pragma unroll
+          for (int al = 0; al < G::NA; ++al) {
+            const int src = (lane & ~3) | ((al & 7) >> 1);
+#pragma unroll
+            for (int v = 0; v < nv; ++v) {
+              const double d = __shfl_sync(0xffffffffu, dv[v][al >> 3][al & 1], src);
+              bq[v] = fma(c_t.scale[al], d * d, bq[v]);
+            }
+          }
+          if (k4 == 0) {
+#pragma unroll
+            for (int v = 0; v < nv; ++v) sCw[(q * nv + v) * 8 + r8] = bq[v];
+          }
+#pragma unroll
+          for (int u = 0; u < nv; ++u)
+#pragma unroll
+            for (int n = 0; n < ND; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+          ++q;
+        }
+      }
+    }
+    __syncwarp();
+    PHASE_MARK(1);
+    // ---- nonlinear weights: lane k4 handles variables v = k4 (+4)
+    for (int v = k4; v < nv; v += 4) {
+      double wt[NS];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        const double bb = sCw[(q * nv + v) * 8 + r8];
+        wt[q] = c_t.gamma_lin[q] * (1.0 / fma(bb, bb, c_k.eps));
+      }
+      double sum = wt[0];
+#pragma unroll
+      for (int q = 1; q < NS; ++q) sum = sum + wt[q];
+      const double inv_sum = 1.0 / sum;
+      const double c0 = (wt[0] * inv_sum) * c_t.inv_g0;
+      sCw[v * 8 + r8] = c0;
+#pragma unroll
+      for (int q = 1; q < NS; ++q)
+        sCw[(q * nv + v) * 8 + r8] = fma(-c0, c_t.gamma_lin[q], wt[q] * inv_sum);
+    }
+    __syncwarp();
+    PHASE_MARK(2);
+    // ---- pass 2: face-point columns, Phi, WENO-AO combination
+    double V[nv][NPT][2];
+    {
+      double acc[nv][NPT][2];
+#pragma unroll
+      for (int u = 0; u < nv; ++u)
+#pragma unroll
+        for (int n = 0; n < NPT; ++n) acc[u][n][0] = acc[u][n][1] = V[u][n][0] = V[u][n][1] = 0.0;
+      int q = 0;
+      // software pipeline: fragments of chunk ck+1 load while chunk ck issues
+      double av[nv], bv[NPT];
+      {
+        const int inpl = sTab[2 * k4], oz = sTab[2 * k4 + 1];
+        const double* ap = plane(oz + R) + inpl + cidx;
+#pragma unroll
+        for (int u = 0; u < nv; ++u) av[u] = ap[u * C::RROW];
+#pragma unroll
+        for (int n = 0; n < NPT; ++n) bv[n] = sBf[n * 32 + lane];
+      }
+#pragma unroll 1
+      for (int ck = 0; ck < G::NCHUNK; ++ck) {
+        const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
+        const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
+        const double* ap = plane(oz + R) + inpl + cidx;
+        double an[nv], bn[NPT];
+#pragma unroll
+        for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
+#pragma unroll
+        for (int n = 0; n < NPT; ++n) bn[n] = sBf[(cn * NPT + n) * 32 + lane];
+#pragma unroll
+        for (int n = 0; n < NPT; ++n)
+#pragma unroll
+          for (int u = 0; u < nv; ++u) dmma(acc[u][n][0], acc[u][n][1], av[u], bv[n]);
+#pragma unroll
+        for (int u = 0; u < nv; ++u) av[u] = an[u];
+#pragma unroll
+        for (int n = 0; n < NPT; ++n) bv[n] = bn[n];
+        if (sQ[ck] & 256) {
+          double cq[nv];
+#pragma unroll
+          for (int v = 0; v < nv; ++v) cq[v] = sCw[(q * nv + v) * 8 + r8];
+#pragma unroll
+          for (int n = 0; n < NPT; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              double X[nv];
+#pragma unroll
+              for (int u = 0; u < nv; ++u) X[u] = acc[u][n][e];
+#pragma unroll
+              for (int v = 0; v < nv; ++v) {
+                const double wv_ = phi_row<D>(T, X, v);
+                V[v][n][e] = q == 0 ? cq[v] * wv_ : fma(cq[v], wv_, V[v][n][e]);
+              }
+            }
+#pragma unroll
+          for (int u = 0; u < nv; ++u)
+#pragma unroll
+            for (int n = 0; n < NPT; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+          ++q;
+        }
+      }
+    }
+    PHASE_MARK(3);
+    // ---- Phi^-1: conservative states at this lane's points s = 8n + 2k4 + e
+    double st[NPT][2][nv];
+#pragma unroll
+    for (int n = 0; n < NPT; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double Wp[nv];
+#pragma unroll
+        for (int v = 0; v < nv; ++v) Wp[v] = V[v][n][e];
+        d_from_recon(D, T, c_k.inv_gm1, Wp, st[n][e]);
+      }
+    // ---- positivity limiter: neighbourhood statistics, the 4
+    // lanes of the quad split the 3^d neighbours and reduce (max/min exact)
+    double rbmax = T.rt, rbmin = T.rt, pbmin = pr0[icn], cmin = pr0[C::PROW + icn];
+    {
+      constexpr int NN = D == 3 ? 27 : 9;
+      for (int m = k4; m < NN; m += 4) {
+        const int aa = m % 3 - 1;
+        const int bb = D == 3 ? (m / 3) % 3 - 1 : 0;
+        const int cc = D == 3 ? m / 9 - 1 : m / 3 - 1;
+        const double r = plane(R + cc)[(D == 3 ? bb * C::RX : 0) + icr + aa];
+        const double* prz = cc < 0 ? prm : (cc > 0 ? prp : pr0);
+        const int ip = (D == 3 ? bb * C::NX : 0) + icn + aa;
+        rbmax = fmax(rbmax, r);
+        rbmin = fmin(rbmin, r);
+        pbmin = fmin(pbmin, prz[ip]);
+        cmin = fmin(cmin, prz[C::PROW + ip]);
+      }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        rbmax = fmax(rbmax, __shfl_xor_sync(0xffffffffu, rbmax, o));
+        rbmin = fmin(rbmin, __shfl_xor_sync(0xffffffffu, rbmin, o));
+        pbmin = fmin(pbmin, __shfl_xor_sync(0xffffffffu, pbmin, o));
+        cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+      }
+    }
+    double delta = 0.5 * (pr0[3 * C::PROW + icn + 1] - pr0[3 * C::PROW + icn - 1]);
+    if (D == 3) {
+      delta = fma(0.5, pr0[4 * C::PROW + icn + C::NX] - pr0[4 * C::PROW + icn - C::NX], delta);
+      delta = fma(0.5, prp[5 * C::PROW + icn] - prm[5 * C::PROW + icn], delta);
+    } else {
+      delta = fma(0.5, prp[4 * C::PROW + icn] - prm[4 * C::PROW + icn], delta);
+    }
+    const double kc = c_k.kf * cmin;
+    double eta = -(delta + kc) / kc;
+    eta = fmin(1.0, fmax(0.0, eta));
+    const double fup = fma(c_k.kappa, 1.0 - eta, 1.0);
+    const double flo = fma(-c_k.kappa, 1.0 - eta, 1.0);
+    const double rmax = rbmax * fup, rmin = rbmin * flo, pmin = pbmin * flo;
+    const double rt = T.rt, pt = pr0[icn];
+    if (!(rt > 0.0) || !(pt > 0.0) || !(rmin > 0.0) || !(pmin > 0.0))
+      if (active && k4 == 0) atomicOr(err, 2);
+    double Ubar[nv];
+    Ubar[0] = rt;
+#pragma unroll
+    for (int d = 0; d < D; ++d) Ubar[1 + d] = T.mt[d];
+    Ubar[nv - 1] = plane(R)[(nv - 1) * C::RROW + icr];
+    double th = 1.0;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (8 * n + 2 * k4 + e < NP) {
+          const double r = st[n][e][0];
+          if (r < rmin)
+            th = fmin(th, (rt - rmin) / (rt - r));
+          else if (r > rmax)
+            th = fmin(th, (rmax - rt) / (r - rt));
+        }
+    th = fmin(th, __shfl_xor_sync(0xffffffffu, th, 1));
+    th = fmin(th, __shfl_xor_sync(0xffffffffu, th, 2));
+    if (th < 1.0) {
+#pragma unroll
+      for (int n = 0; n < NPT; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int v = 0; v < nv; ++v) st[n][e][v] = fma(th, st[n][e][v] - Ubar[v], Ubar[v]);
+    }
+    double thp = 1.0;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (8 * n + 2 * k4 + e < NP && d_p_below(D, st[n][e], c_k.gm1, pmin)) {
+          StateV<D> a_, b_;
+#pragma unroll
+          for (int v = 0; v < nv; ++v) {
+            a_.v[v] = st[n][e][v];
+            b_.v[v] = Ubar[v];
+          }
+          thp = fmin(thp, theta_p_bisect<D>(a_, b_, pmin));
+        }
+    thp = fmin(thp, __shfl_xor_sync(0xffffffffu, thp, 1));
+    thp = fmin(thp, __shfl_xor_sync(0xffffffffu, thp, 2));
+    if (active) {
+      const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
+#pragma unroll
+      for (int n = 0; n < NPT; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int sp = 8 * n + 2 * k4 + e;
+          if (sp < NP) {
+#pragma unroll
+            for (int v = 0; v < nv; ++v) {
+              const double u = thp < 1.0 ? fma(thp, st[n][e][v] - Ubar[v], Ubar[v]) : st[n][e][v];
+              St[(long long)(sp * nv + v) * ch.next + tid] = u;
+            }
+          }
+        }
+    }
+    PHASE_MARK(4);
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    PHASE_MARK(5);
+  }
+}
+
+#endif
