@@ -180,69 +180,6 @@ void weno_field(const kfvm_table* t, const Consts& k, const double* g, double* b
   }
 }
 
-// WENO-AO of one cell for all variables, in "U-space" form:
-// every derivative / face-point vector is contracted with the RAW conserved
-// variables of the stencil (stencil-order fma chains), and the linear map
-// Phi (constant part dropped) is applied to each vector of nv
-// contractions.  Mathematically identical to reconstructing W = Phi U cell by
-// cell; this is the pinned order the GPU tensor-core path reproduces.
-void weno_cell_u(const kfvm_table* t, const Consts& k, const Transform& T,
-                 const double* const* cells, double* W /* [np][nv] */,
-                 double* beta_out /* [NS][nv] or null */) {
-  const int NS = t->n_stencils, nv = k.nv, dim = k.dim;
-  double c[KFVM_MAX_STENCILS][5];
-  double wt[KFVM_MAX_STENCILS][5];
-  for (int q = 0; q < NS; ++q) {
-    const int N = t->size[q];
-    const int* gat = t->gather + t->cell_offset[q];
-    const double* Dq = t->deriv + (size_t)t->cell_offset[q] * t->n_alpha;
-    double beta[5] = {0, 0, 0, 0, 0};
-    for (int a = 0; a < t->n_alpha; ++a) {
-      double D[5];
-      for (int u = 0; u < nv; ++u) {
-        double acc = 0.0;
-        for (int h = 0; h < N; ++h) acc = fma(Dq[a * N + h], cells[gat[h]][u], acc);
-        D[u] = acc;
-      }
-      for (int v = 0; v < nv; ++v) {
-        const double dv = to_recon(dim, T, k.gm1, D, v);
-        beta[v] = fma(k.scale[a], dv * dv, beta[v]);
-      }
-    }
-    for (int v = 0; v < nv; ++v) {
-      if (beta_out) beta_out[q * nv + v] = beta[v];
-      wt[q][v] = t->gamma_lin[q] * (1.0 / fma(beta[v], beta[v], k.eps));
-    }
-  }
-  const double inv_g0 = 1.0 / t->gamma_lin[0];
-  for (int v = 0; v < nv; ++v) {
-    double sum = wt[0][v];
-    for (int q = 1; q < NS; ++q) sum = sum + wt[q][v];
-    const double inv_sum = 1.0 / sum;
-    c[0][v] = (wt[0][v] * inv_sum) * inv_g0;
-    for (int q = 1; q < NS; ++q) c[q][v] = fma(-c[0][v], t->gamma_lin[q], wt[q][v] * inv_sum);
-  }
-  for (int s = 0; s < t->n_points; ++s) {
-    double val[5] = {0, 0, 0, 0, 0};
-    for (int q = 0; q < NS; ++q) {
-      const int N = t->size[q];
-      const int* gat = t->gather + t->cell_offset[q];
-      const double* r = t->face + (size_t)t->cell_offset[q] * t->n_points + (size_t)s * N;
-      double P[5];
-      for (int u = 0; u < nv; ++u) {
-        double acc = 0.0;
-        for (int h = 0; h < N; ++h) acc = fma(r[h], cells[gat[h]][u], acc);
-        P[u] = acc;
-      }
-      for (int v = 0; v < nv; ++v) {
-        const double w = to_recon(dim, T, k.gm1, P, v);
-        val[v] = (q == 0) ? c[0][v] * w : fma(c[q][v], w, val[v]);
-      }
-    }
-    for (int v = 0; v < nv; ++v) W[s * nv + v] = val[v];
-  }
-}
-
 // ------------------------------------------------------- positivity limiter
 // nbr: 3^dim averages (i fastest), centre at index (3^dim)/2.  Returns 0 ok,
 // 2 if the cell average itself is inadmissible.
@@ -494,8 +431,13 @@ int cell_states(const kfvm_table* t, const Consts& k, const Slab& S, int i, int 
   std::vector<const double*> cells(N0);
   for (int h = 0; h < N0; ++h)
     cells[h] = S.at(i + t->offsets[3 * h], j + t->offsets[3 * h + 1], kk + t->offsets[3 * h + 2]);
+  double g[128], vals[64];
   double W[64 * 5];
-  weno_cell_u(t, k, T, cells.data(), W, nullptr);
+  for (int v = 0; v < nv; ++v) {  // W = Phi U cell by cell, then WENO-AO per variable
+    for (int h = 0; h < N0; ++h) g[h] = to_recon(dim, T, k.gm1, cells[h], v);
+    weno_field(t, k, g, nullptr, nullptr, vals);
+    for (int s = 0; s < np; ++s) W[s * nv + v] = vals[s];
+  }
   for (int s = 0; s < np; ++s) from_recon(dim, T, k.inv_gm1, W + s * nv, st + s * nv);
   double nbr[27 * 5];
   const int kr = dim == 3 ? 1 : 0;

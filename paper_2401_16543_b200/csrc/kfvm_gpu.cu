@@ -394,7 +394,7 @@ struct kfvm_handle {
   cudaGraphExec_t graph = nullptr;
   bool timing = false;
   bool fast = true;
-  int engine = 2;  // 0 generic (k_states), 2 tensor-core U-space (k_states_u)
+  int engine = 2;  // 0 generic (k_states), 1 unrolled DFMA (k_states_fast), 2 tensor core (k_states_u)
   int kz = 16;     // planes marched by one k_states_u CTA
   double *d_Bd = nullptr, *d_Bf = nullptr;
   int* d_gat4 = nullptr;
@@ -458,6 +458,10 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
       const long long nblk2 = (long long)((ch.ex + 31) / 32) * ch.em * ((ch.ep + KZ - 1) / KZ);
       k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
           U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4);
+    } else if (h->engine == 1) {
+      const long long nblk = (long long)((ch.ex + 31) / 32) * ch.em * ch.ep;
+      k_states_fast<DIM, R><<<(unsigned)nblk, 32 * (DIM + 2), 0, h->stream>>>(U, h->Pr, h->St, h->g,
+                                                                            ch, h->d_err);
     } else {
       k_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
                                                                     h->d_err);
@@ -647,6 +651,8 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   for (int i = 0; i < G::NTOT; ++i)
     if (t->gather[i] != G::GATHER[i])
       return fail(h, KFVM_ERR_CONFIG, "table substencils differ from kfvm_gen.cuh");
+  CK(cudaMemcpyToSymbol(G::face_symbol(), t->face, sizeof(double) * G::NTOT * G::NP));
+  CK(cudaMemcpyToSymbol(G::deriv_symbol(), t->deriv, sizeof(double) * G::NTOT * G::NA));
   // DMMA operands: per 4-entry chunk of each stencil (zero-padded at the
   // front), B fragments in lane order (k = lane%4, column = lane/4) and the
   // S0 position of every chunk slot
@@ -717,7 +723,8 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   h->R = cfg->radius;
   h->nv = cfg->dim + 2;
   h->NP = t->n_points;
-  h->engine = 2;
+  // measured: unrolled DFMA for 2-D, tensor cores for 3-D
+  h->engine = cfg->dim == 2 ? 1 : 2;
   h->kz = 16;
   if (dist) {
     h->rank = dist->rank;
@@ -1111,7 +1118,7 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
   std::string n(name ? name : "");
   if (n == "fast_states" || n == "engine") {
     if (n == "engine") {
-      if (value != 0 && value != 2) return fail(h, KFVM_ERR_CONFIG, "engine must be 0 or 2");
+      if (value < 0 || value > 2) return fail(h, KFVM_ERR_CONFIG, "engine: 0 generic, 1 DFMA, 2 tensor core");
       h->engine = (int)value;
     } else {
       h->engine = value ? 2 : 0;

@@ -1,18 +1,20 @@
 // kfvm_recon_u.cuh — reconstruct_states on the FP64 tensor cores,
-// "U-space" form, plane-marching CTAs with a cp.async ring buffer.
+// plane-marching CTAs with a cp.async ring buffer.
 // Included inside namespace kfvm_b200 by kfvm_gpu.cu.
 //
-// Contract (oracle weno_cell_u): every derivative / face-point
-// vector of every (sub)stencil is contracted with the RAW conserved
-// variables (stencil-order fma chains, here as zero-padded 4-entry DMMA
-// chunks: mma.sync.m8n8k4.f64 == the sequential fma chain, measured), then
-// the linear map Phi is applied to the vector of nv contractions.
+// Contract (oracle weno_field): the stencil values are the
+// linearized primitives W = Phi U of the central cell; every derivative /
+// face-point vector of every (sub)stencil is contracted with them in
+// stencil-order fma chains, here as zero-padded 4-entry DMMA chunks
+// (mma.sync.m8n8k4.f64 == the sequential fma chain, measured).  In the A
+// fragment, lane (r8, k4) holds row r8 = its own cell, so each lane applies
+// its own cell's Phi to the raw U it loads.
 //
 // Work decomposition.  CTA = 4 warps = a 32-cell x-segment of one row; it
 // marches along the slab axis over KZ extended planes.  Warp w owns cells
 // w, w+4, .., w+28 of the segment and ALL variables: the DMMA A operand (8 cells x 4
-// stencil entries) is read straight from the staged U region, B (4 entries
-// x 8 columns) is the weight table in fragment order.  The accumulator layout
+// stencil entries) is transformed on the fly from the staged U region, B (4
+// entries x 8 columns) is the weight table in fragment order.  The accumulator layout
 // puts all nv variables of one (cell, column) in one thread, so Phi, the
 // WENO-AO combination, Phi^-1 and the positivity limiter run in registers;
 // the 4 lanes of a quad share a cell and reduce with shuffles.
@@ -210,28 +212,21 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
         for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
 #pragma unroll
         for (int n = 0; n < ND; ++n) bn[n] = sBd[(cn * ND + n) * 32 + lane];
+        double aw[nv];  // W = Phi U at the slot, with this lane's cell's Phi
+#pragma unroll
+        for (int v = 0; v < nv; ++v) aw[v] = phi_row<D>(T, av, v);
 #pragma unroll
         for (int n = 0; n < ND; ++n)
 #pragma unroll
-          for (int u = 0; u < nv; ++u) dmma(acc[u][n][0], acc[u][n][1], av[u], bv[n]);
+          for (int v = 0; v < nv; ++v) dmma(acc[v][n][0], acc[v][n][1], aw[v], bv[n]);
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
         for (int n = 0; n < ND; ++n) bv[n] = bn[n];
         if (sQ[ck] & 256) {
-          // acc[u][n][e]: cell r8, alpha = 8n + 2k4 + e; Phi per (alpha), then
+          // acc[v][n][e]: variable v of cell r8, alpha = 8n + 2k4 + e;
           // beta_v = sequential chain over alpha (quad shuffles)
-          double dv[nv][ND][2];
-#pragma unroll
-          for (int n = 0; n < ND; ++n)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              double X[nv];
-#pragma unroll
-              for (int u = 0; u < nv; ++u) X[u] = acc[u][n][e];
-#pragma unroll
-              for (int v = 0; v < nv; ++v) dv[v][n][e] = phi_row<D>(T, X, v);
-            }
+          double (&dv)[nv][ND][2] = acc;
           double bq[nv];
 #pragma unroll
           for (int v = 0; v < nv; ++v) bq[v] = 0.0;
@@ -307,10 +302,13 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
         for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
 #pragma unroll
         for (int n = 0; n < NPT; ++n) bn[n] = sBf[(cn * NPT + n) * 32 + lane];
+        double aw[nv];  // W = Phi U at the slot, with this lane's cell's Phi
+#pragma unroll
+        for (int v = 0; v < nv; ++v) aw[v] = phi_row<D>(T, av, v);
 #pragma unroll
         for (int n = 0; n < NPT; ++n)
 #pragma unroll
-          for (int u = 0; u < nv; ++u) dmma(acc[u][n][0], acc[u][n][1], av[u], bv[n]);
+          for (int v = 0; v < nv; ++v) dmma(acc[v][n][0], acc[v][n][1], aw[v], bv[n]);
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
@@ -322,16 +320,10 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
 #pragma unroll
           for (int n = 0; n < NPT; ++n)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              double X[nv];
+            for (int e = 0; e < 2; ++e)
 #pragma unroll
-              for (int u = 0; u < nv; ++u) X[u] = acc[u][n][e];
-#pragma unroll
-              for (int v = 0; v < nv; ++v) {
-                const double wv_ = phi_row<D>(T, X, v);
-                V[v][n][e] = q == 0 ? cq[v] * wv_ : fma(cq[v], wv_, V[v][n][e]);
-              }
-            }
+              for (int v = 0; v < nv; ++v)
+                V[v][n][e] = q == 0 ? cq[v] * acc[v][n][e] : fma(cq[v], acc[v][n][e], V[v][n][e]);
 #pragma unroll
           for (int u = 0; u < nv; ++u)
 #pragma unroll

@@ -133,7 +133,7 @@ def test_engines_bitwise_identical(require_gpu, idx, n):
     """generic / unrolled-DFMA / DMMA reconstruction engines agree bit for bit."""
     g, ic, U, rset = _setup(idx, n, {})
     outs = []
-    for eng in (0, 2):
+    for eng in (0, 1, 2):
         with K.Solver(g, rset) as s:
             s.set_option("engine", eng)
             s.set_state(U)

@@ -1,13 +1,23 @@
 #!/usr/bin/env python
-"""Generate paper_2401_16543_b200/csrc/kfvm_gen.cuh — the compile-time stencil
-structure of the KFVM-WENO reconstruction for (dim, R) in {(2,2), (2,3), (3,2)}:
-the offsets of the full stencil S0 (lexicographic by (k, j, i),
-proj/core/src/geometry.cpp:10-20), the substencil gathers (geometry.cpp:22-34,
-PAPER.md §3.1), the sizes and the number of 4-entry DMMA chunks per stencil.
+"""Generate paper_2401_16543_b200/csrc/kfvm_gen.cuh — fully unrolled sparse
+stencil contractions of the KFVM-WENO reconstruction for (dim, R) in
+{(2,2), (2,3), (3,2)}.
 
-The structure follows from the geometry alone; the weight values are
-uploaded at run time from the binary128 table, and kfvm_gpu_create checks the
-table's gather/offset arrays against the structure compiled in here.
+The generated code is the device form of the oracle's weno_field
+(oracle/kfvm_oracle.cpp): for every (sub)stencil q it evaluates the n_alpha
+derivative dot products (beta_q), the nonlinear weights
+and, for every face point s, the WENO-AO combination of the per-stencil point
+values, each dot product accumulated in stencil order from 0.0 with
+explicit fma — the pinned FP contract.  Because the gather pattern is known at
+compile time, the stencil values live in registers and every weight is a
+__constant__ operand with a literal offset (DFMA R, R, c[bank][imm], R): the
+inner loop issues nothing but DFMAs.
+
+Only the sparsity structure is generated (it follows from the stencil
+geometry, proj/core/src/geometry.cpp:10-34 and PAPER.md §3.1); the weight
+values are uploaded at run time from the binary128 table, and
+kfvm_gpu_create checks the table's gather/offset arrays against the
+structure compiled in here.
 """
 from __future__ import annotations
 
@@ -69,6 +79,8 @@ def gen_case(dim, R):
     tag = f"{dim}{R}"
     L = []
     L.append(f"// ---- dim={dim} R={R}: N0={len(full)} sizes={sizes} n_alpha={na} n_points={npnt}")
+    L.append(f"__constant__ __align__(16) double c_f{tag}[{total * npnt}];  // table.face, [q][s][h]")
+    L.append(f"__constant__ __align__(16) double c_d{tag}[{total * na}];  // table.deriv, [q][a][h]")
     L.append(f"template <> struct Gen<{dim}, {R}> {{")
     L.append(f"  static constexpr int N0 = {len(full)}, NP = {npnt}, NA = {na}, NS = {ns}, NTOT = {total};")
     L.append(f"  static constexpr int OFF[{len(full)}][3] = {{" +
@@ -86,6 +98,55 @@ def gen_case(dim, R):
     L.append("  __host__ __device__ static constexpr int kc(int q) { return (qsize(q) + 3) / 4; }")
     L.append("  __host__ __device__ static constexpr int cbase(int q) { return q == 0 ? 0 : cbase(q - 1) + kc(q - 1); }")
     L.append(f"  static constexpr int NCHUNK = {sum((n + 3) // 4 for n in sizes)};")
+    L.append("  static const void* face_symbol() { return (const void*)&c_f%s; }" % tag)
+    L.append("  static const void* deriv_symbol() { return (const void*)&c_d%s; }" % tag)
+    # WENO body, fully unrolled: stencil values in registers, every weight a
+    # __constant__ operand with a literal offset (table layouts [q][a][h] and
+    # [q][s][h]); each dot product is the stencil-order fma chain from 0.0.
+    L.append("  // beta_q, omega_q, WENO-AO values of one scalar field g on S0")
+    L.append("  static __device__ __forceinline__ void weno(const double (&g)[%d], double (&w)[%d],"
+             % (len(full), npnt))
+    L.append("                                              const double* __restrict__ sc,")
+    L.append("                                              const double* __restrict__ gam, double eps,")
+    L.append("                                              double inv_g0) {")
+    for q in range(ns):
+        m, N, o = members[q], sizes[q], offs[q]
+        L.append(f"    double wt{q};")
+        L.append("    {")
+        L.append("      double b = 0.0;")
+        for a in range(na):
+            base = o * na + a * N
+            L.append("      {")
+            L.append("        double d = 0.0;")
+            for hh, h in enumerate(m):
+                L.append(f"        d = fma(c_d{tag}[{base + hh}], g[{h}], d);")
+            L.append(f"        b = fma(sc[{a}], d * d, b);")
+            L.append("      }")
+        L.append(f"      wt{q} = gam[{q}] * (1.0 / fma(b, b, eps));")
+        L.append("    }")
+    L.append("    double sum = wt0;")
+    for q in range(1, ns):
+        L.append(f"    sum = sum + wt{q};")
+    L.append("    const double inv_sum = 1.0 / sum;")
+    for q in range(ns):
+        L.append(f"    const double om{q} = wt{q} * inv_sum;")
+    L.append("    const double c0 = om0 * inv_g0;")
+    for q in range(1, ns):
+        L.append(f"    const double c{q} = fma(-c0, gam[{q}], om{q});")
+    for s_ in range(npnt):
+        L.append("    {")
+        for q in range(ns):
+            m, N, o = members[q], sizes[q], offs[q]
+            base = o * npnt + s_ * N
+            L.append(f"      double p{q} = 0.0;")
+            for hh, h in enumerate(m):
+                L.append(f"      p{q} = fma(c_f{tag}[{base + hh}], g[{h}], p{q});")
+        L.append("      double v = c0 * p0;")
+        for q in range(1, ns):
+            L.append(f"      v = fma(c{q}, p{q}, v);")
+        L.append(f"      w[{s_}] = v;")
+        L.append("    }")
+    L.append("  }")
     L.append("};")
     return "\n".join(L)
 
