@@ -34,7 +34,7 @@ $(BUILD)/kfvm_ic.o: $(SRC)/kfvm_ic.cpp $(SRC)/kfvm_ic_eval.h $(SRC)/kfvm_ic_host
 $(SRC)/kfvm_gen.cuh: tools/gen_kernels.py
 	python tools/gen_kernels.py
 
-$(BUILD)/kfvm_gpu.o: $(SRC)/kfvm_gpu.cu $(SRC)/kfvm_gen.cuh $(SRC)/kfvm_device.cuh $(SRC)/kfvm_ic_eval.h include/kfvm_b200.h | $(BUILD)
+$(BUILD)/kfvm_gpu.o: $(SRC)/kfvm_gpu.cu $(SRC)/kfvm_gen.cuh $(SRC)/kfvm_device.cuh $(SRC)/kfvm_recon.cuh $(SRC)/kfvm_recon_u.cuh $(SRC)/kfvm_ic_eval.h include/kfvm_b200.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_kfvm_gpu.txt || (cat $(BUILD)/ptxas_kfvm_gpu.txt; false)
 
 $(LIB): $(BUILD)/kfvm_table.o $(BUILD)/kfvm_ic.o $(BUILD)/kfvm_gpu.o

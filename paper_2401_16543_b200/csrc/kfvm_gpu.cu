@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -402,6 +403,7 @@ struct kfvm_handle {
   double t_states = 0, t_flux = 0, t_update = 0, t_other = 0;
   nccl_comm comm = nullptr;
   long long launches = 0;
+  long long graph_launches = 0;
   long long st_budget = 16LL << 30;
   std::string err;
 };
@@ -449,16 +451,35 @@ void toc(kfvm_handle* h, double* acc) {
   *acc += ms;
 }
 
+// KFVM_DEBUG_SYNC=1: synchronise after each launch outside graph capture and
+// report the first failing kernel (debugging aid; off by default)
+void dbg_sync(kfvm_handle* h, const char* what) {
+  static const bool on = getenv("KFVM_DEBUG_SYNC") != nullptr;
+  if (!on) return;
+  cudaStreamCaptureStatus cs;
+  cudaStreamIsCapturing(h->stream, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return;
+  const cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) fprintf(stderr, "[kfvm] %s: %s\n", what, cudaGetErrorString(e));
+}
+
 template <int DIM, int R>
 void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   tic(h);
-  if constexpr (!(DIM == 3 && R == 3)) {
-    if (h->engine == 2) {
-      const int KZ = h->kz;
-      const long long nblk2 = (long long)((ch.ex + 31) / 32) * ch.em * ((ch.ep + KZ - 1) / KZ);
-      k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
-          U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4);
-    } else if (h->engine == 1) {
+  if (h->engine == 2) {
+    const int KZ = h->kz;
+    const long long nblk2 = (long long)((ch.ex + 31) / 32) * ch.em * ((ch.ep + KZ - 1) / KZ);
+    k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
+        U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4);
+    dbg_sync(h, "k_states_u");
+    if (UCfg<DIM, R>::NG > 1) {
+      h->launches++;
+      k_limit_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
+                                                                          h->d_err);
+      dbg_sync(h, "k_limit_states");
+    }
+  } else if constexpr (Gen<DIM, R>::UNROLLED) {
+    if (h->engine == 1) {
       const long long nblk = (long long)((ch.ex + 31) / 32) * ch.em * ch.ep;
       k_states_fast<DIM, R><<<(unsigned)nblk, 32 * (DIM + 2), 0, h->stream>>>(U, h->Pr, h->St, h->g,
                                                                             ch, h->d_err);
@@ -651,22 +672,29 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   for (int i = 0; i < G::NTOT; ++i)
     if (t->gather[i] != G::GATHER[i])
       return fail(h, KFVM_ERR_CONFIG, "table substencils differ from kfvm_gen.cuh");
-  CK(cudaMemcpyToSymbol(G::face_symbol(), t->face, sizeof(double) * G::NTOT * G::NP));
-  CK(cudaMemcpyToSymbol(G::deriv_symbol(), t->deriv, sizeof(double) * G::NTOT * G::NA));
+  if constexpr (G::UNROLLED) {
+    CK(cudaMemcpyToSymbol(G::face_symbol(), t->face, sizeof(double) * G::NTOT * G::NP));
+    CK(cudaMemcpyToSymbol(G::deriv_symbol(), t->deriv, sizeof(double) * G::NTOT * G::NA));
+  }
   // DMMA operands: per 4-entry chunk of each stencil (zero-padded at the
   // front), B fragments in lane order (k = lane%4, column = lane/4) and the
   // S0 position of every chunk slot
   using M = UCfg<D, R>;
   std::vector<double> bd((size_t)G::NCHUNK * M::ND * 32, 0.0), bf((size_t)G::NCHUNK * M::NPT * 32, 0.0);
-  std::vector<int> g4((size_t)G::NCHUNK * 5, 0);  // gather rows, then sQ (stencil | last<<8)
+  // per chunk slot {region offset in the plane, z offset}, then sQ (stencil | last<<8)
+  std::vector<int> g4((size_t)G::NCHUNK * 9, 0);
   for (int q = 0, ck = 0; q < G::NS; ++q) {
     const int N = t->size[q], o = t->cell_offset[q];
     const int kcq = (N + 3) / 4, pad = 4 * kcq - N;
     for (int jj = 0; jj < kcq; ++jj, ++ck) {
-      g4[(size_t)G::NCHUNK * 4 + ck] = q | (jj == kcq - 1 ? 256 : 0);
+      g4[(size_t)G::NCHUNK * 8 + ck] = q | (jj == kcq - 1 ? 256 : 0);
       for (int k = 0; k < 4; ++k) {
         const int hh = 4 * jj + k - pad;
-        g4[(size_t)ck * 4 + k] = t->gather[o + (hh < 0 ? 0 : hh)];
+        const int e = t->gather[o + (hh < 0 ? 0 : hh)];
+        const int ox = G::OFF[e][0], oy = D == 3 ? G::OFF[e][1] : 0;
+        const int oz = D == 3 ? G::OFF[e][2] : G::OFF[e][1];
+        g4[(size_t)(ck * 4 + k) * 2] = (oy + (D == 3 ? R : 0)) * M::RX + ox + R;
+        g4[(size_t)(ck * 4 + k) * 2 + 1] = oz;
       }
       for (int lane = 0; lane < 32; ++lane) {
         const int k = lane % 4, col = lane / 4, hh = 4 * jj + k - pad;
@@ -725,6 +753,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   h->NP = t->n_points;
   // measured: unrolled DFMA for 2-D, tensor cores for 3-D
   h->engine = cfg->dim == 2 ? 1 : 2;
+  h->kz = cfg->dim == 3 && cfg->radius == 3 ? 32 : 16;
   h->kz = 16;
   if (dist) {
     h->rank = dist->rank;
@@ -829,6 +858,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     if (cfg->dim == 2 && cfg->radius == 2) rc = upload_gen<2, 2>(h, t);
     if (cfg->dim == 2 && cfg->radius == 3) rc = upload_gen<2, 3>(h, t);
     if (cfg->dim == 3 && cfg->radius == 2) rc = upload_gen<3, 2>(h, t);
+    if (cfg->dim == 3 && cfg->radius == 3) rc = upload_gen<3, 3>(h, t);
   }
   const size_t ufull = (size_t)h->g.vstride * h->nv;
   bad(cudaMalloc(&h->U0, ufull * sizeof(double)), "cudaMalloc U0");
@@ -1031,15 +1061,11 @@ extern "C" int kfvm_gpu_run_async(kfvm_handle* h, int nsteps) {
     if (e != cudaSuccess) return fail(h, KFVM_ERR_DEVICE, "graph capture failed");
     CK(cudaGraphInstantiate(&h->graph, graph, 0));
     cudaGraphDestroy(graph);
+    h->graph_launches = h->launches - l0;  // kernels in one captured step
     h->launches = l0;
   }
-  long long per_step = 0;
-  {
-    const int nchunks = (h->g.np_loc + h->chunk - 1) / h->chunk;
-    per_step = 1 + 3 * (2 + 3LL * nchunks);
-  }
   for (int s = 0; s < nsteps; ++s) CK(cudaGraphLaunch(h->graph, h->stream));
-  h->launches += per_step * nsteps;
+  h->launches += h->graph_launches * nsteps;
   return KFVM_OK;
 }
 

@@ -44,7 +44,10 @@ struct UCfg {
   static constexpr int PPL = NF * PROW;
   static constexpr int PRING = 4;
   static constexpr int SCW = G::NS * nv * 8;            // beta / c_q per warp
-  static constexpr int SB = G::NCHUNK * (ND + NPT) * 32;  // B fragments
+  static constexpr bool BSMEM = G::NCHUNK * (ND + NPT) * 32 * 8 <= 48 * 1024;
+  static constexpr int SB = BSMEM ? G::NCHUNK * (ND + NPT) * 32 : 0;  // B fragments
+  static constexpr int PG = NPT <= 3 ? NPT : 4;         // point tiles per pass-2 group
+  static constexpr int NG = (NPT + PG - 1) / PG;         // groups (>1: limiter separate)
   static constexpr size_t bytes() {
     return sizeof(double) * (RING * PL + PRING * PPL + 4 * SCW + SB) +
            sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK);
@@ -78,23 +81,19 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
   double* sC = sPr + C::PRING * C::PPL;          // [warp][q][v][8]
   double* sBd = sC + 4 * C::SCW;                 // B fragments [chunk][n][lane]
   double* sBf = sBd + G::NCHUNK * ND * 32;
-  int* sTab = reinterpret_cast<int*>(sBf + G::NCHUNK * NPT * 32);  // [chunk][4] {inplane, oz}
+  int* sTab = reinterpret_cast<int*>(sBd + C::SB);  // [chunk][4] {inplane, oz}
   int* sQ = sTab + 8 * G::NCHUNK;                        // stencil | last << 8
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int k4 = lane & 3, r8 = lane >> 2;
-  // chunk tables: region offsets of every chunk slot
-  for (int i = threadIdx.x; i < 4 * G::NCHUNK; i += 128) {
-    const int h = gat4[i];
-    const int ox = G::off(h, 0);
-    const int oy = D == 3 ? G::off(h, 1) : 0;
-    const int oz = D == 3 ? G::off(h, 2) : G::off(h, 1);
-    sTab[2 * i] = (oy + (D == 3 ? R : 0)) * C::RX + ox + R;
-    sTab[2 * i + 1] = oz;
+  // chunk tables (host-built): region offset and z offset of every chunk slot
+  for (int i = threadIdx.x; i < 9 * G::NCHUNK; i += 128) sTab[i] = gat4[i];
+  if constexpr (C::BSMEM) {
+    for (int i = threadIdx.x; i < G::NCHUNK * ND * 32; i += 128) sBd[i] = __ldg(Bd + i);
+    for (int i = threadIdx.x; i < G::NCHUNK * NPT * 32; i += 128) sBf[i] = __ldg(Bf + i);
   }
-  for (int i = threadIdx.x; i < G::NCHUNK; i += 128) sQ[i] = gat4[4 * G::NCHUNK + i];
-  for (int i = threadIdx.x; i < G::NCHUNK * ND * 32; i += 128) sBd[i] = __ldg(Bd + i);
-  for (int i = threadIdx.x; i < G::NCHUNK * NPT * 32; i += 128) sBf[i] = __ldg(Bf + i);
+  const double* Bdp = C::BSMEM ? sBd : Bd;
+  const double* Bfp = C::BSMEM ? sBf : Bf;
 
   const int nseg = (ch.ex + 31) >> 5;
   int bid = blockIdx.x;
@@ -200,7 +199,7 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = ap[u * C::RROW];
 #pragma unroll
-        for (int n = 0; n < ND; ++n) bv[n] = sBd[n * 32 + lane];
+        for (int n = 0; n < ND; ++n) bv[n] = Bdp[n * 32 + lane];
       }
 #pragma unroll 1
       for (int ck = 0; ck < G::NCHUNK; ++ck) {
@@ -211,7 +210,7 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
 #pragma unroll
         for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
 #pragma unroll
-        for (int n = 0; n < ND; ++n) bn[n] = sBd[(cn * ND + n) * 32 + lane];
+        for (int n = 0; n < ND; ++n) bn[n] = Bdp[(cn * ND + n) * 32 + lane];
         double aw[nv];  // W = Phi U at the slot, with this lane's cell's Phi
 #pragma unroll
         for (int v = 0; v < nv; ++v) aw[v] = phi_row<D>(T, av, v);
@@ -273,52 +272,59 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
     }
     __syncwarp();
     PHASE_MARK(2);
-    // ---- pass 2: face-point columns, Phi, WENO-AO combination
-    double V[nv][NPT][2];
-    {
-      double acc[nv][NPT][2];
+    // ---- pass 2: face-point columns, WENO-AO combination; point tiles in
+    // groups of PG (registers); with more than one group the limited states
+    // are produced by k_limit_states from the unlimited ones stored here
+    constexpr int PG = C::PG, NG = C::NG;
+    double V[nv][PG][2];
+#pragma unroll
+    for (int grp = 0; grp < NG; ++grp) {
+      const int t0 = grp * PG;
+      double acc[nv][PG][2];
 #pragma unroll
       for (int u = 0; u < nv; ++u)
 #pragma unroll
-        for (int n = 0; n < NPT; ++n) acc[u][n][0] = acc[u][n][1] = V[u][n][0] = V[u][n][1] = 0.0;
+        for (int n = 0; n < PG; ++n) acc[u][n][0] = acc[u][n][1] = V[u][n][0] = V[u][n][1] = 0.0;
       int q = 0;
       // software pipeline: fragments of chunk ck+1 load while chunk ck issues
-      double av[nv], bv[NPT];
+      double av[nv], bv[PG];
       {
         const int inpl = sTab[2 * k4], oz = sTab[2 * k4 + 1];
         const double* ap = plane(oz + R) + inpl + cidx;
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = ap[u * C::RROW];
 #pragma unroll
-        for (int n = 0; n < NPT; ++n) bv[n] = sBf[n * 32 + lane];
+        for (int n = 0; n < PG; ++n) bv[n] = t0 + n < NPT ? Bfp[(t0 + n) * 32 + lane] : 0.0;
       }
 #pragma unroll 1
       for (int ck = 0; ck < G::NCHUNK; ++ck) {
         const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
         const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
         const double* ap = plane(oz + R) + inpl + cidx;
-        double an[nv], bn[NPT];
+        double an[nv], bn[PG];
 #pragma unroll
         for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
 #pragma unroll
-        for (int n = 0; n < NPT; ++n) bn[n] = sBf[(cn * NPT + n) * 32 + lane];
+        for (int n = 0; n < PG; ++n)
+          bn[n] = t0 + n < NPT ? Bfp[(cn * NPT + t0 + n) * 32 + lane] : 0.0;
         double aw[nv];  // W = Phi U at the slot, with this lane's cell's Phi
 #pragma unroll
         for (int v = 0; v < nv; ++v) aw[v] = phi_row<D>(T, av, v);
 #pragma unroll
-        for (int n = 0; n < NPT; ++n)
+        for (int n = 0; n < PG; ++n)
+          if (t0 + n < NPT)
 #pragma unroll
-          for (int v = 0; v < nv; ++v) dmma(acc[v][n][0], acc[v][n][1], aw[v], bv[n]);
+            for (int v = 0; v < nv; ++v) dmma(acc[v][n][0], acc[v][n][1], aw[v], bv[n]);
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
-        for (int n = 0; n < NPT; ++n) bv[n] = bn[n];
+        for (int n = 0; n < PG; ++n) bv[n] = bn[n];
         if (sQ[ck] & 256) {
           double cq[nv];
 #pragma unroll
           for (int v = 0; v < nv; ++v) cq[v] = sCw[(q * nv + v) * 8 + r8];
 #pragma unroll
-          for (int n = 0; n < NPT; ++n)
+          for (int n = 0; n < PG; ++n)
 #pragma unroll
             for (int e = 0; e < 2; ++e)
 #pragma unroll
@@ -327,12 +333,33 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
 #pragma unroll
           for (int u = 0; u < nv; ++u)
 #pragma unroll
-            for (int n = 0; n < NPT; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+            for (int n = 0; n < PG; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
           ++q;
+        }
+      }
+      if constexpr (NG > 1) {
+        // unlimited states of this group (Phi^-1); k_limit_states limits them
+        if (active) {
+          const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
+#pragma unroll
+          for (int n = 0; n < PG; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int sp = 8 * (t0 + n) + 2 * k4 + e;
+              if (t0 + n < NPT && sp < NP) {
+                double Wp[nv], u5[nv];
+#pragma unroll
+                for (int v = 0; v < nv; ++v) Wp[v] = V[v][n][e];
+                d_from_recon(D, T, c_k.inv_gm1, Wp, u5);
+#pragma unroll
+                for (int v = 0; v < nv; ++v) St[(long long)(sp * nv + v) * ch.next + tid] = u5[v];
+              }
+            }
         }
       }
     }
     PHASE_MARK(3);
+    if constexpr (NG == 1) {
     // ---- Phi^-1: conservative states at this lane's points s = 8n + 2k4 + e
     double st[NPT][2][nv];
 #pragma unroll
@@ -444,11 +471,93 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
           }
         }
     }
+    }
     PHASE_MARK(4);
     __pipeline_wait_prior(0);
     __syncthreads();
     PHASE_MARK(5);
   }
+}
+
+// ------------------------------------------------------- k_limit_states
+// Positivity limiter over the stored face states of one
+// extended cell, for the configurations whose points do not fit the
+// registers of k_states_u (3-D R=3).  Same arithmetic as the fused epilogue.
+template <int D, int R>
+__global__ void __launch_bounds__(128) k_limit_states(const double* __restrict__ U,
+                                                      const double* __restrict__ Pr,
+                                                      double* __restrict__ St, Geo g, Chunk ch,
+                                                      int* __restrict__ err) {
+  constexpr int nv = D + 2, NP = Gen<D, R>::NP;
+  const long long tid = (long long)blockIdx.x * 128 + threadIdx.x;
+  if (tid >= ch.next) return;
+  const int a = (int)(tid % ch.ex);
+  const long long r1 = tid / ch.ex;
+  const int b = (int)(r1 % ch.em), c = (int)(r1 / ch.em);
+  const int x = a - 1, j = D == 3 ? b - 1 : 0, p = ch.c0 - 1 + c;
+  const long long ic = uidx<D>(g, x, j, p);
+  double Ubar[nv];
+#pragma unroll
+  for (int v = 0; v < nv; ++v) Ubar[v] = __ldg(U + v * g.vstride + ic);
+  double rbmax = Ubar[0], rbmin = Ubar[0], pbmin = __ldg(Pr + ic), cmin = __ldg(Pr + g.vstride + ic);
+  for (int cc = -1; cc <= 1; ++cc)
+    for (int bb = (D == 3 ? -1 : 0); bb <= (D == 3 ? 1 : 0); ++bb)
+      for (int aa = -1; aa <= 1; ++aa) {
+        const long long o = uidx<D>(g, x + aa, j + bb, p + cc);
+        const double r = __ldg(U + o);
+        rbmax = fmax(rbmax, r);
+        rbmin = fmin(rbmin, r);
+        pbmin = fmin(pbmin, __ldg(Pr + o));
+        cmin = fmin(cmin, __ldg(Pr + g.vstride + o));
+      }
+  double delta = 0.5 * (__ldg(Pr + 3 * g.vstride + uidx<D>(g, x + 1, j, p)) -
+                        __ldg(Pr + 3 * g.vstride + uidx<D>(g, x - 1, j, p)));
+  if (D == 3) {
+    delta = fma(0.5, __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j + 1, p)) -
+                         __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j - 1, p)), delta);
+    delta = fma(0.5, __ldg(Pr + 5 * g.vstride + uidx<D>(g, x, j, p + 1)) -
+                         __ldg(Pr + 5 * g.vstride + uidx<D>(g, x, j, p - 1)), delta);
+  } else {
+    delta = fma(0.5, __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j, p + 1)) -
+                         __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j, p - 1)), delta);
+  }
+  const double kc = c_k.kf * cmin;
+  double eta = -(delta + kc) / kc;
+  eta = fmin(1.0, fmax(0.0, eta));
+  const double fup = fma(c_k.kappa, 1.0 - eta, 1.0);
+  const double flo = fma(-c_k.kappa, 1.0 - eta, 1.0);
+  const double rmax = rbmax * fup, rmin = rbmin * flo, pmin = pbmin * flo;
+  const double rt = Ubar[0], pt = __ldg(Pr + ic);
+  if (!(rt > 0.0) || !(pt > 0.0) || !(rmin > 0.0) || !(pmin > 0.0)) atomicOr(err, 2);
+  double th = 1.0;
+  for (int sp = 0; sp < NP; ++sp) {
+    const double r = St[(long long)(sp * nv) * ch.next + tid];
+    if (r < rmin)
+      th = fmin(th, (rt - rmin) / (rt - r));
+    else if (r > rmax)
+      th = fmin(th, (rmax - rt) / (r - rt));
+  }
+  double thp = 1.0;
+  for (int sp = 0; sp < NP; ++sp) {
+    StateV<D> a_, b_;
+#pragma unroll
+    for (int v = 0; v < nv; ++v) {
+      const double u = St[(long long)(sp * nv + v) * ch.next + tid];
+      a_.v[v] = th < 1.0 ? fma(th, u - Ubar[v], Ubar[v]) : u;
+      b_.v[v] = Ubar[v];
+    }
+    if (d_p_below(D, a_.v, c_k.gm1, pmin)) thp = fmin(thp, theta_p_bisect<D>(a_, b_, pmin));
+  }
+  if (th < 1.0 || thp < 1.0)
+    for (int sp = 0; sp < NP; ++sp)
+#pragma unroll
+      for (int v = 0; v < nv; ++v) {
+        double* q = St + (long long)(sp * nv + v) * ch.next + tid;
+        double u = *q;
+        if (th < 1.0) u = fma(th, u - Ubar[v], Ubar[v]);
+        if (thp < 1.0) u = fma(thp, u - Ubar[v], Ubar[v]);
+        *q = u;
+      }
 }
 
 #endif

@@ -128,7 +128,7 @@ def test_runtime_error_on_inadmissible_state(require_gpu):
             s.advance(1)
 
 
-@pytest.mark.parametrize("idx,n", [(1, 20), (2, 24), (3, 10), (4, 10)])
+@pytest.mark.parametrize("idx,n", [(1, 20), (2, 24), (3, 10), (4, 10), (5, 10)])
 def test_engines_bitwise_identical(require_gpu, idx, n):
     """generic / unrolled-DFMA / DMMA reconstruction engines agree bit for bit."""
     g, ic, U, rset = _setup(idx, n, {})

@@ -27,7 +27,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "paper_2401_16543_b200", "csrc", "kfvm_gen.cuh")
 
-CASES = [(2, 2), (2, 3), (3, 2)]
+CASES = [(2, 2), (2, 3), (3, 2), (3, 3)]
+# (3,3): structure only — its 198 KB of weights exceed __constant__ and its
+# unrolled contractions (25k fma per variable) would not fit the I-cache
+UNROLLED = {(2, 2), (2, 3), (3, 2)}
 
 
 def full_stencil(dim, R):
@@ -79,8 +82,10 @@ def gen_case(dim, R):
     tag = f"{dim}{R}"
     L = []
     L.append(f"// ---- dim={dim} R={R}: N0={len(full)} sizes={sizes} n_alpha={na} n_points={npnt}")
-    L.append(f"__constant__ __align__(16) double c_f{tag}[{total * npnt}];  // table.face, [q][s][h]")
-    L.append(f"__constant__ __align__(16) double c_d{tag}[{total * na}];  // table.deriv, [q][a][h]")
+    unrolled = (dim, R) in UNROLLED
+    if unrolled:
+        L.append(f"__constant__ __align__(16) double c_f{tag}[{total * npnt}];  // table.face, [q][s][h]")
+        L.append(f"__constant__ __align__(16) double c_d{tag}[{total * na}];  // table.deriv, [q][a][h]")
     L.append(f"template <> struct Gen<{dim}, {R}> {{")
     L.append(f"  static constexpr int N0 = {len(full)}, NP = {npnt}, NA = {na}, NS = {ns}, NTOT = {total};")
     L.append(f"  static constexpr int OFF[{len(full)}][3] = {{" +
@@ -98,6 +103,10 @@ def gen_case(dim, R):
     L.append("  __host__ __device__ static constexpr int kc(int q) { return (qsize(q) + 3) / 4; }")
     L.append("  __host__ __device__ static constexpr int cbase(int q) { return q == 0 ? 0 : cbase(q - 1) + kc(q - 1); }")
     L.append(f"  static constexpr int NCHUNK = {sum((n + 3) // 4 for n in sizes)};")
+    L.append(f"  static constexpr bool UNROLLED = {'true' if unrolled else 'false'};")
+    if not unrolled:
+        L.append("};")
+        return "\n".join(L)
     L.append("  static const void* face_symbol() { return (const void*)&c_f%s; }" % tag)
     L.append("  static const void* deriv_symbol() { return (const void*)&c_d%s; }" % tag)
     # WENO body, fully unrolled: stencil values in registers, every weight a
