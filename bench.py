@@ -293,7 +293,7 @@ def main():
     for _ in range(e2e_steps):
         s.set_state(Uh)
         s.ssp_rk3_step()
-        Uh[...] = s.get_state()
+        s.get_state(out=Uh)
     t_e2e = time.perf_counter() - t0
     if dist:
         t = torch.tensor([t_e2e], dtype=torch.float64)

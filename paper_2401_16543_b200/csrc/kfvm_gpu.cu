@@ -944,10 +944,7 @@ extern "C" int kfvm_gpu_set_state_device(kfvm_handle* h, const double* U_dev) {
   k_transpose<0><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, const_cast<double*>(U_dev), h->g,
                                                          h->nv);
   h->launches++;
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  // the captured step graph reads the fixed state buffers: it stays valid
   CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return KFVM_OK;

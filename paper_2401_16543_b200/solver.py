@@ -106,8 +106,16 @@ class Solver:
             raise ValueError("state size does not match the rank's slab")
         self._check(self.L.kfvm_gpu_set_state(self.h, U.ctypes.data), "set_state")
 
-    def get_state(self) -> np.ndarray:
-        U = np.empty(self.local_shape, dtype=np.float64)
+    def get_state(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """The rank's state (AoS); into ``out`` (C-contiguous float64, e.g. a
+        pinned buffer) when given."""
+        if out is None:
+            U = np.empty(self.local_shape, dtype=np.float64)
+        else:
+            if (out.dtype != np.float64 or not out.flags.c_contiguous
+                    or out.size != self.local_cells * self.grid.nvar):
+                raise ValueError("out must be a C-contiguous float64 array of the slab's size")
+            U = out
         self._check(self.L.kfvm_gpu_get_state(self.h, U.ctypes.data), "get_state")
         return U
 

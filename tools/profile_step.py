@@ -11,11 +11,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--steps", type=int, default=1)
-ap.add_argument("--fast", type=int, default=1)
+ap.add_argument("--engine", type=int, default=-1, help="-1: the solver default")
 a = ap.parse_args()
 w = K.baseline_config(a.config, n=a.n)
 with K.Solver(w.grid) as s:
-    s.set_option("fast_states", a.fast)
+    if a.engine >= 0:
+        s.set_option("engine", a.engine)
     s.generate_ic(w.ic)
     d = s.advance(a.steps)
     print("ok", w.grid.shape, d)
