@@ -205,6 +205,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", type=int, default=None,
                     help="reconstruction kernel: 0 generic, 1 DFMA, 2 DMMA (default: per dim)")
+    ap.add_argument("--kz", type=int, default=None,
+                    help="slab-axis planes marched by one reconstruction CTA (engines 2, 3)")
     args = ap.parse_args()
 
     import paper_2401_16543_b200 as K
@@ -235,6 +237,8 @@ def main():
     stream = torch.cuda.ExternalStream(s.stream)
     if args.engine is not None:
         s.set_option("engine", args.engine)
+    if args.kz is not None:
+        s.set_option("kz", args.kz)
 
     # warm-up (also captures the CUDA graph)
     s.generate_ic(w.ic)

@@ -82,6 +82,7 @@ constexpr int npoints(int dim, int R) { return dim == 2 ? 4 * R : 6 * R * R; }
 
 #include "kfvm_recon.cuh"
 #include "kfvm_recon_u.cuh"
+#include "kfvm_recon_row.cuh"
 
 // ------------------------------------------------------------------ k_flux
 template <int DIM>
@@ -90,12 +91,44 @@ __device__ __forceinline__ long long sidx(const Chunk& ch, int x, int j, int p) 
   return ((long long)(p + 1) * ch.em + (DIM == 3 ? j + 1 : 0)) * ch.ex + (x + 1);
 }
 
+// Flux of one face (Riemann solve at its R^(d-1) GL points, quadrature in
+// point order): direction d, face box position (a, b, c), F index f.
 template <int DIM, int R>
-__global__ void __launch_bounds__(128) k_flux(const double* __restrict__ St,
-                                              double* __restrict__ F, Geo g, Chunk ch) {
+__device__ __forceinline__ void face_flux(const double* __restrict__ St, double* __restrict__ F,
+                                          const Chunk& ch, int d, int a, int b, int c,
+                                          long long f) {
   constexpr int nv = DIM + 2;
   constexpr int NP = npoints(DIM, R);
   constexpr int RP = NP / (2 * DIM);
+  const bool slab = d == DIM - 1;
+  const bool mid = DIM == 3 && d == 1;
+  const int x = a, j = DIM == 3 ? b : 0, p = c;
+  const int lx = x - (d == 0), lj = j - (mid ? 1 : 0), lp = p - (slab ? 1 : 0);
+  const long long iL = sidx<DIM>(ch, lx, lj, lp);
+  const long long iR = sidx<DIM>(ch, x, j, p);
+  double Fb[nv];
+#pragma unroll
+  for (int v = 0; v < nv; ++v) Fb[v] = 0.0;
+  for (int m = 0; m < RP; ++m) {
+    const int sL = (2 * d + 1) * RP + m;
+    const int sR = (2 * d) * RP + m;
+    double UL[nv], UR[nv], Fp[nv];
+#pragma unroll
+    for (int v = 0; v < nv; ++v) {
+      UL[v] = St[(long long)(sL * nv + v) * ch.next + iL];
+      UR[v] = St[(long long)(sR * nv + v) * ch.next + iR];
+    }
+    d_riemann<DIM>(c_k, d, UL, UR, Fp);
+#pragma unroll
+    for (int v = 0; v < nv; ++v) Fb[v] = fma(c_t.face_w[sR], Fp[v], Fb[v]);
+  }
+#pragma unroll
+  for (int v = 0; v < nv; ++v) F[(long long)(d * nv + v) * ch.nfb + f] = Fb[v];
+}
+
+template <int DIM, int R>
+__global__ void __launch_bounds__(128) k_flux(const double* __restrict__ St,
+                                              double* __restrict__ F, Geo g, Chunk ch) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= ch.nfb) return;
   const int a = (int)(tid % ch.fx);
@@ -103,34 +136,34 @@ __global__ void __launch_bounds__(128) k_flux(const double* __restrict__ St,
   const int b = (int)(r1 % ch.fm);
   const int c = (int)(r1 / ch.fm);
   const int nm = DIM == 3 ? g.nm : 1;
+#pragma unroll
   for (int d = 0; d < DIM; ++d) {
     const bool slab = d == DIM - 1;
     const bool mid = DIM == 3 && d == 1;
     const bool valid = (d == 0 ? true : a < g.nx) && (mid ? true : (DIM == 3 ? b < nm : true)) &&
                        (slab ? true : c < ch.C);
-    if (!valid) continue;
-    const int x = a, j = DIM == 3 ? b : 0, p = c;
-    const int lx = x - (d == 0), lj = j - (mid ? 1 : 0), lp = p - (slab ? 1 : 0);
-    const long long iL = sidx<DIM>(ch, lx, lj, lp);
-    const long long iR = sidx<DIM>(ch, x, j, p);
-    double Fb[nv];
-#pragma unroll
-    for (int v = 0; v < nv; ++v) Fb[v] = 0.0;
-    for (int m = 0; m < RP; ++m) {
-      const int sL = (2 * d + 1) * RP + m;
-      const int sR = (2 * d) * RP + m;
-      double UL[nv], UR[nv], Fp[nv];
-#pragma unroll
-      for (int v = 0; v < nv; ++v) {
-        UL[v] = St[(long long)(sL * nv + v) * ch.next + iL];
-        UR[v] = St[(long long)(sR * nv + v) * ch.next + iR];
-      }
-      d_riemann<DIM>(c_k, d, UL, UR, Fp);
-#pragma unroll
-      for (int v = 0; v < nv; ++v) Fb[v] = fma(c_t.face_w[sR], Fp[v], Fb[v]);
-    }
-#pragma unroll
-    for (int v = 0; v < nv; ++v) F[(long long)(d * nv + v) * ch.nfb + tid] = Fb[v];
+    if (valid) face_flux<DIM, R>(St, F, ch, d, a, b, c, tid);
+  }
+}
+
+// Fluxes of the faces on the tile edges of the fused 2-D stage kernel
+// (k_stage_row): x-faces a = 32k+31 (between two x-segments) and y-faces
+// c = KZ k + KZ-1 (between two row blocks); their states were stored in St.
+template <int R>
+__global__ void __launch_bounds__(128) k_flux_edges(const double* __restrict__ St,
+                                                    double* __restrict__ F, Geo g, Chunk ch,
+                                                    int KZ) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nxb = g.nx >= 31 ? (g.nx - 31) / 32 + 1 : 0;
+  const int nyb = ch.C >= KZ - 1 ? (ch.C - (KZ - 1)) / KZ + 1 : 0;
+  const long long nx_faces = (long long)nxb * ch.C;
+  if (tid < nx_faces) {
+    const int a = 32 * (int)(tid % nxb) + 31, c = (int)(tid / nxb);
+    face_flux<2, R>(St, F, ch, 0, a, 0, c, (long long)c * ch.fx + a);
+  } else if (tid < nx_faces + (long long)nyb * g.nx) {
+    const long long t = tid - nx_faces;
+    const int a = (int)(t % g.nx), c = KZ * (int)(t / g.nx) + KZ - 1;
+    face_flux<2, R>(St, F, ch, 1, a, 0, c, (long long)c * ch.fx + a);
   }
 }
 
@@ -466,6 +499,29 @@ void dbg_sync(kfvm_handle* h, const char* what) {
 template <int DIM, int R>
 void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   tic(h);
+  if constexpr (DIM == 2) {
+    if (h->engine == 3) {
+      // fused states + interior face fluxes, then the tile-edge faces
+      const int KZ = h->kz;
+      const long long nblk3 = (long long)((ch.ex + 31) / 32) * ((ch.ep + KZ - 1) / KZ);
+      k_stage_row<R><<<(unsigned)nblk3, 128, 0, h->stream>>>(U, h->Pr, h->St, h->F, h->g, ch, KZ,
+                                                             h->d_err);
+      dbg_sync(h, "k_stage_row");
+      h->launches++;
+      toc(h, &h->t_states);
+      tic(h);
+      const long long nxb = h->g.nx >= 31 ? (h->g.nx - 31) / 32 + 1 : 0;
+      const long long nyb = ch.C >= KZ - 1 ? (ch.C - (KZ - 1)) / KZ + 1 : 0;
+      const long long ne = nxb * ch.C + nyb * h->g.nx;
+      if (ne > 0) {
+        k_flux_edges<R><<<blocks(ne, 128), 128, 0, h->stream>>>(h->St, h->F, h->g, ch, KZ);
+        dbg_sync(h, "k_flux_edges");
+        h->launches++;
+      }
+      toc(h, &h->t_flux);
+      return;
+    }
+  }
   if (h->engine == 2) {
     const int KZ = h->kz;
     const long long nblk2 = (long long)((ch.ex + 31) / 32) * ch.em * ((ch.ep + KZ - 1) / KZ);
@@ -754,7 +810,6 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   // measured: unrolled DFMA for 2-D, tensor cores for 3-D
   h->engine = cfg->dim == 2 ? 1 : 2;
   h->kz = cfg->dim == 3 && cfg->radius == 3 ? 32 : 16;
-  h->kz = 16;
   if (dist) {
     h->rank = dist->rank;
     h->nranks = dist->nranks;
@@ -1141,7 +1196,9 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
   std::string n(name ? name : "");
   if (n == "fast_states" || n == "engine") {
     if (n == "engine") {
-      if (value < 0 || value > 2) return fail(h, KFVM_ERR_CONFIG, "engine: 0 generic, 1 DFMA, 2 tensor core");
+      if (value < 0 || value > 3 || (value == 3 && h->dim != 2))
+        return fail(h, KFVM_ERR_CONFIG,
+                    "engine: 0 generic, 1 DFMA, 2 tensor core, 3 DFMA row-marching (2-D)");
       h->engine = (int)value;
     } else {
       h->engine = value ? 2 : 0;

@@ -130,10 +130,11 @@ def test_runtime_error_on_inadmissible_state(require_gpu):
 
 @pytest.mark.parametrize("idx,n", [(1, 20), (2, 24), (3, 10), (4, 10), (5, 10)])
 def test_engines_bitwise_identical(require_gpu, idx, n):
-    """generic / unrolled-DFMA / DMMA reconstruction engines agree bit for bit."""
+    """generic / unrolled-DFMA / DMMA / row-marching DFMA reconstruction engines agree
+    bit for bit."""
     g, ic, U, rset = _setup(idx, n, {})
     outs = []
-    for eng in (0, 1, 2):
+    for eng in ((0, 1, 2, 3) if g.dim == 2 else (0, 1, 2)):
         with K.Solver(g, rset) as s:
             s.set_option("engine", eng)
             s.set_state(U)
