@@ -93,10 +93,9 @@ __device__ __forceinline__ long long sidx(const Chunk& ch, int x, int j, int p) 
 
 // Flux of one face (Riemann solve at its R^(d-1) GL points, quadrature in
 // point order): direction d, face box position (a, b, c), F index f.
-template <int DIM, int R>
+template <int DIM, int R, int d>
 __device__ __forceinline__ void face_flux(const double* __restrict__ St, double* __restrict__ F,
-                                          const Chunk& ch, int d, int a, int b, int c,
-                                          long long f) {
+                                          const Chunk& ch, int a, int b, int c, long long f) {
   constexpr int nv = DIM + 2;
   constexpr int NP = npoints(DIM, R);
   constexpr int RP = NP / (2 * DIM);
@@ -118,7 +117,7 @@ __device__ __forceinline__ void face_flux(const double* __restrict__ St, double*
       UL[v] = St[(long long)(sL * nv + v) * ch.next + iL];
       UR[v] = St[(long long)(sR * nv + v) * ch.next + iR];
     }
-    d_riemann<DIM>(c_k, d, UL, UR, Fp);
+    d_riemann_dir<DIM, d>(c_k, UL, UR, Fp);
 #pragma unroll
     for (int v = 0; v < nv; ++v) Fb[v] = fma(c_t.face_w[sR], Fp[v], Fb[v]);
   }
@@ -126,24 +125,33 @@ __device__ __forceinline__ void face_flux(const double* __restrict__ St, double*
   for (int v = 0; v < nv; ++v) F[(long long)(d * nv + v) * ch.nfb + f] = Fb[v];
 }
 
+#ifndef KFVM_FLUX_MINB
+#define KFVM_FLUX_MINB 1
+#endif
+// one thread per face of direction d = blockIdx.y
 template <int DIM, int R>
-__global__ void __launch_bounds__(128) k_flux(const double* __restrict__ St,
-                                              double* __restrict__ F, Geo g, Chunk ch) {
+__global__ void __launch_bounds__(128, KFVM_FLUX_MINB) k_flux(const double* __restrict__ St,
+                                                              double* __restrict__ F, Geo g,
+                                                              Chunk ch) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= ch.nfb) return;
+  const int d = blockIdx.y;
   const int a = (int)(tid % ch.fx);
   const long long r1 = tid / ch.fx;
   const int b = (int)(r1 % ch.fm);
   const int c = (int)(r1 / ch.fm);
   const int nm = DIM == 3 ? g.nm : 1;
-#pragma unroll
-  for (int d = 0; d < DIM; ++d) {
-    const bool slab = d == DIM - 1;
-    const bool mid = DIM == 3 && d == 1;
-    const bool valid = (d == 0 ? true : a < g.nx) && (mid ? true : (DIM == 3 ? b < nm : true)) &&
-                       (slab ? true : c < ch.C);
-    if (valid) face_flux<DIM, R>(St, F, ch, d, a, b, c, tid);
-  }
+  const bool slab = d == DIM - 1;
+  const bool mid = DIM == 3 && d == 1;
+  const bool valid = (d == 0 ? true : a < g.nx) && (mid ? true : (DIM == 3 ? b < nm : true)) &&
+                     (slab ? true : c < ch.C);
+  if (!valid) return;
+  if (d == 0)
+    face_flux<DIM, R, 0>(St, F, ch, a, b, c, tid);
+  else if (d == 1)
+    face_flux<DIM, R, 1>(St, F, ch, a, b, c, tid);
+  else
+    face_flux<DIM, R, DIM == 3 ? 2 : 1>(St, F, ch, a, b, c, tid);
 }
 
 // Fluxes of the faces on the tile edges of the fused 2-D stage kernel
@@ -159,11 +167,11 @@ __global__ void __launch_bounds__(128) k_flux_edges(const double* __restrict__ S
   const long long nx_faces = (long long)nxb * ch.C;
   if (tid < nx_faces) {
     const int a = 32 * (int)(tid % nxb) + 31, c = (int)(tid / nxb);
-    face_flux<2, R>(St, F, ch, 0, a, 0, c, (long long)c * ch.fx + a);
+    face_flux<2, R, 0>(St, F, ch, a, 0, c, (long long)c * ch.fx + a);
   } else if (tid < nx_faces + (long long)nyb * g.nx) {
     const long long t = tid - nx_faces;
     const int a = (int)(t % g.nx), c = KZ * (int)(t / g.nx) + KZ - 1;
-    face_flux<2, R>(St, F, ch, 1, a, 0, c, (long long)c * ch.fx + a);
+    face_flux<2, R, 1>(St, F, ch, a, 0, c, (long long)c * ch.fx + a);
   }
 }
 
@@ -550,7 +558,8 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   h->launches++;
   toc(h, &h->t_states);
   tic(h);
-  k_flux<DIM, R><<<blocks(ch.nfb, 128), 128, 0, h->stream>>>(h->St, h->F, h->g, ch);
+  k_flux<DIM, R><<<dim3((unsigned)blocks(ch.nfb, 128), DIM), 128, 0, h->stream>>>(h->St, h->F,
+                                                                                 h->g, ch);
   h->launches++;
   toc(h, &h->t_flux);
 }
