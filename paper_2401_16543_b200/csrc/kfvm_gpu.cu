@@ -125,12 +125,10 @@ __device__ __forceinline__ void face_flux(const double* __restrict__ St, double*
   for (int v = 0; v < nv; ++v) F[(long long)(d * nv + v) * ch.nfb + f] = Fb[v];
 }
 
-#ifndef KFVM_FLUX_MINB
-#define KFVM_FLUX_MINB 1
-#endif
-// one thread per face of direction d = blockIdx.y
+// one thread per face of direction d = blockIdx.y; min blocks per SM
+// measured on config 2 (8) and config 3 (6)
 template <int DIM, int R>
-__global__ void __launch_bounds__(128, KFVM_FLUX_MINB) k_flux(const double* __restrict__ St,
+__global__ void __launch_bounds__(128, DIM == 2 ? 8 : 6) k_flux(const double* __restrict__ St,
                                                               double* __restrict__ F, Geo g,
                                                               Chunk ch) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
