@@ -205,6 +205,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", type=int, default=None,
                     help="reconstruction kernel: 0 generic, 1 DFMA, 2 DMMA (default: per dim)")
+    ap.add_argument("--opt", action="append", default=[], metavar="NAME=VALUE",
+                    help="extra solver option (kfvm_gpu_set_option), e.g. overlap=1")
     ap.add_argument("--kz", type=int, default=None,
                     help="slab-axis planes marched by one reconstruction CTA (engines 2, 3)")
     args = ap.parse_args()
@@ -239,6 +241,9 @@ def main():
         s.set_option("engine", args.engine)
     if args.kz is not None:
         s.set_option("kz", args.kz)
+    for o in args.opt:
+        k, v = o.split("=")
+        s.set_option(k, int(v))
 
     # warm-up (also captures the CUDA graph)
     s.generate_ic(w.ic)

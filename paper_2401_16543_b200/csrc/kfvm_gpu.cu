@@ -52,6 +52,7 @@ struct Chunk {
   long long next;         // extended cells
   int fx, fm, fp;         // face box extents
   long long nfb;          // face-box cells
+  int e0, e1;             // extended planes whose states a states launch computes
 };
 
 __device__ __forceinline__ int remap(int i, int n, int bc) {
@@ -431,6 +432,9 @@ struct kfvm_handle {
   double* d_tt = nullptr;  // {t, t_end} for advance_to
   int *d_step = nullptr, *d_err = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t s_halo = nullptr;     // halo exchange, overlapped with interior planes
+  cudaEvent_t ev_fork = nullptr, ev_halo = nullptr;
+  int overlap = 0;                   // split each stage into interior / border planes
   cudaGraphExec_t graph = nullptr;
   bool timing = false;
   bool fast = true;
@@ -462,6 +466,8 @@ int fail(kfvm_handle* h, int code, const std::string& msg) {
   } while (0)
 
 inline unsigned blocks(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+// extended cells of the planes [e0, e1) a states launch covers
+inline long long ext_range(const Chunk& ch) { return (long long)ch.ex * ch.em * (ch.e1 - ch.e0); }
 
 Chunk make_chunk(const kfvm_handle* h, int c0, int C) {
   Chunk ch;
@@ -470,6 +476,8 @@ Chunk make_chunk(const kfvm_handle* h, int c0, int C) {
   ch.ex = h->g.nx + 2;
   ch.em = h->dim == 3 ? h->g.nm + 2 : 1;
   ch.ep = C + 2;
+  ch.e0 = 0;
+  ch.e1 = ch.ep;
   ch.next = (long long)ch.ex * ch.em * ch.ep;
   ch.fx = h->g.nx + 1;
   ch.fm = h->dim == 3 ? h->g.nm + 1 : 1;
@@ -530,31 +538,36 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   }
   if (h->engine == 2) {
     const int KZ = h->kz;
-    const long long nblk2 = (long long)((ch.ex + 31) / 32) * ch.em * ((ch.ep + KZ - 1) / KZ);
+    const long long nblk2 =
+        (long long)((ch.ex + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
     k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
         U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4);
     dbg_sync(h, "k_states_u");
     if (UCfg<DIM, R>::NG > 1) {
       h->launches++;
-      k_limit_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
+      k_limit_states<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
                                                                           h->d_err);
       dbg_sync(h, "k_limit_states");
     }
   } else if constexpr (Gen<DIM, R>::UNROLLED) {
     if (h->engine == 1) {
-      const long long nblk = (long long)((ch.ex + 31) / 32) * ch.em * ch.ep;
+      const long long nblk = (long long)((ch.ex + 31) / 32) * ch.em * (ch.e1 - ch.e0);
       k_states_fast<DIM, R><<<(unsigned)nblk, 32 * (DIM + 2), 0, h->stream>>>(U, h->Pr, h->St, h->g,
                                                                             ch, h->d_err);
     } else {
-      k_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
-                                                                    h->d_err);
+      k_states<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g,
+                                                                          ch, h->d_err);
     }
   } else {
-    k_states<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
-                                                                  h->d_err);
+    k_states<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g,
+                                                                        ch, h->d_err);
   }
   h->launches++;
   toc(h, &h->t_states);
+}
+
+template <int DIM, int R>
+void launch_flux(kfvm_handle* h, const Chunk& ch) {
   tic(h);
   k_flux<DIM, R><<<dim3((unsigned)blocks(ch.nfb, 128), DIM), 128, 0, h->stream>>>(h->St, h->F,
                                                                                  h->g, ch);
@@ -562,11 +575,28 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   toc(h, &h->t_flux);
 }
 
-void states_and_flux(kfvm_handle* h, const double* U, const Chunk& ch) {
+// states of the chunk's extended planes [ch.e0, ch.e1) (the fused 2-D
+// engine also produces the face fluxes)
+void states_only(kfvm_handle* h, const double* U, const Chunk& ch) {
   if (h->dim == 2 && h->R == 2) launch_states<2, 2>(h, U, ch);
   if (h->dim == 2 && h->R == 3) launch_states<2, 3>(h, U, ch);
   if (h->dim == 3 && h->R == 2) launch_states<3, 2>(h, U, ch);
   if (h->dim == 3 && h->R == 3) launch_states<3, 3>(h, U, ch);
+}
+
+bool fused_engine(const kfvm_handle* h) { return h->dim == 2 && h->engine == 3; }
+
+void flux_only(kfvm_handle* h, const Chunk& ch) {
+  if (fused_engine(h)) return;
+  if (h->dim == 2 && h->R == 2) launch_flux<2, 2>(h, ch);
+  if (h->dim == 2 && h->R == 3) launch_flux<2, 3>(h, ch);
+  if (h->dim == 3 && h->R == 2) launch_flux<3, 2>(h, ch);
+  if (h->dim == 3 && h->R == 3) launch_flux<3, 3>(h, ch);
+}
+
+void states_and_flux(kfvm_handle* h, const double* U, const Chunk& ch) {
+  states_only(h, U, ch);
+  flux_only(h, ch);
 }
 
 void update(kfvm_handle* h, const Chunk& ch, const double* U0, const double* Uk, double* Uout,
@@ -585,11 +615,11 @@ void update(kfvm_handle* h, const Chunk& ch, const double* U0, const double* Uk,
 }
 
 // fill the slab-axis halo planes of U (local copy and/or NCCL exchange)
-int halo(kfvm_handle* h, double* U) {
+int halo(kfvm_handle* h, double* U, cudaStream_t st) {
   const long long per = (long long)h->g.H * h->g.pstride;
   tic(h);
   if (h->nranks == 1) {
-    k_halo_local<<<blocks(2 * per * h->nv, 256), 256, 0, h->stream>>>(U, h->g, h->nv, h->nsa, 3);
+    k_halo_local<<<blocks(2 * per * h->nv, 256), 256, 0, st>>>(U, h->g, h->nv, h->nsa, 3);
     h->launches++;
   } else {
     NcclApi& N = nccl();
@@ -599,7 +629,7 @@ int halo(kfvm_handle* h, double* U) {
     const int plo = (lo + h->nranks) % h->nranks, phi = hi % h->nranks;
     int which = (has_lo ? 0 : 1) | (has_hi ? 0 : 2);
     if (which) {
-      k_halo_local<<<blocks(2 * per * h->nv, 256), 256, 0, h->stream>>>(U, h->g, h->nv, h->nsa,
+      k_halo_local<<<blocks(2 * per * h->nv, 256), 256, 0, st>>>(U, h->g, h->nv, h->nsa,
                                                                          which);
       h->launches++;
     }
@@ -613,10 +643,10 @@ int halo(kfvm_handle* h, double* U) {
       double* top_halo = base + (long long)(h->g.np_loc + h->g.H) * h->g.pstride;
       double* bot_int = base + per;
       double* bot_halo = base;
-      if (has_hi) N.Send(top_int, per, kNcclDouble, phi, h->comm, h->stream);
-      if (has_lo) N.Recv(bot_halo, per, kNcclDouble, plo, h->comm, h->stream);
-      if (has_lo) N.Send(bot_int, per, kNcclDouble, plo, h->comm, h->stream);
-      if (has_hi) N.Recv(top_halo, per, kNcclDouble, phi, h->comm, h->stream);
+      if (has_hi) N.Send(top_int, per, kNcclDouble, phi, h->comm, st);
+      if (has_lo) N.Recv(bot_halo, per, kNcclDouble, plo, h->comm, st);
+      if (has_lo) N.Send(bot_int, per, kNcclDouble, plo, h->comm, st);
+      if (has_hi) N.Recv(top_halo, per, kNcclDouble, phi, h->comm, st);
     }
     if (N.GroupEnd() != 0) return fail(h, KFVM_ERR_DEVICE, "ncclGroupEnd failed");
   }
@@ -633,23 +663,87 @@ int reduce_smax(kfvm_handle* h) {
 }
 
 // one stage: halo, then per chunk states -> flux -> update
-void prims(kfvm_handle* h, const double* U) {
-  const long long n = h->g.vstride;
+// per-cell quantities of slab planes [p0, p1) (p relative to the first
+// interior plane; halo planes are negative / >= np_loc)
+void prims(kfvm_handle* h, const double* U, int p0, int p1) {
+  if (p1 <= p0) return;
+  const long long t0 = (long long)(p0 + h->g.H) * h->g.pstride;
+  const long long n = (long long)(p1 - p0) * h->g.pstride;
   tic(h);
   if (h->dim == 2)
-    k_prims<2><<<blocks(n, 256), 256, 0, h->stream>>>(U, h->Pr, n, h->g.vstride);
+    k_prims<2><<<blocks(n, 256), 256, 0, h->stream>>>(U, h->Pr, t0, n, h->g.vstride);
   else
-    k_prims<3><<<blocks(n, 256), 256, 0, h->stream>>>(U, h->Pr, n, h->g.vstride);
+    k_prims<3><<<blocks(n, 256), 256, 0, h->stream>>>(U, h->Pr, t0, n, h->g.vstride);
   h->launches++;
   toc(h, &h->t_other);
 }
+void prims(kfvm_handle* h, const double* U) { prims(h, U, -h->g.H, h->g.np_loc + h->g.H); }
 
+// states -> flux -> update over the local planes [q0, q1), in scratch-sized chunks
+void run_planes(kfvm_handle* h, const double* Uin, double* Uout, int stage, int q0, int q1) {
+  for (int c0 = q0; c0 < q1; c0 += h->chunk) {
+    const Chunk ch = make_chunk(h, c0, std::min(h->chunk, q1 - c0));
+    states_and_flux(h, Uin, ch);
+    update(h, ch, h->U0, Uin, Uout, stage);
+  }
+}
+
+// One stage.  With overlap on, the halo exchange runs on s_halo while every
+// state whose stencil, limiter neighbourhood and per-cell quantities lie in
+// the rank's own planes is computed: the chunks that do not reach a halo
+// plane, or — when the slab is one chunk — its extended planes
+// [R+1, np-R+1); then the halo planes' per-cell quantities and the rest.
+// Each state is still computed exactly once with unchanged arithmetic, so the
+// results are bit-identical to the serial schedule.
 int run_stage(kfvm_handle* h, const double* Uin, double* Uout, int stage) {
-  int rc = halo(h, const_cast<double*>(Uin));
+  const int np = h->g.np_loc, R = h->R;
+  const int nch = (np + h->chunk - 1) / h->chunk;
+  auto needs_halo = [&](int c0, int C) { return c0 - 1 - R < 0 || c0 + C + R > np - 1; };
+  if (!h->overlap || fused_engine(h) || np < 2 * R + 3) {
+    int rc = halo(h, const_cast<double*>(Uin), h->stream);
+    if (rc) return rc;
+    prims(h, Uin);
+    run_planes(h, Uin, Uout, stage, 0, np);
+    return KFVM_OK;
+  }
+  CK(cudaEventRecord(h->ev_fork, h->stream));
+  CK(cudaStreamWaitEvent(h->s_halo, h->ev_fork, 0));
+  int rc = halo(h, const_cast<double*>(Uin), h->s_halo);
   if (rc) return rc;
-  prims(h, Uin);
-  for (int c0 = 0; c0 < h->g.np_loc; c0 += h->chunk) {
-    const Chunk ch = make_chunk(h, c0, std::min(h->chunk, h->g.np_loc - c0));
+  CK(cudaEventRecord(h->ev_halo, h->s_halo));
+  prims(h, Uin, 0, np);
+  if (nch == 1) {
+    Chunk ch = make_chunk(h, 0, np);
+    ch.e0 = R + 1;
+    ch.e1 = np - R + 1;
+    states_only(h, Uin, ch);
+    CK(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+    prims(h, Uin, -h->g.H, 0);
+    prims(h, Uin, np, np + h->g.H);
+    ch.e0 = 0;
+    ch.e1 = R + 1;
+    states_only(h, Uin, ch);
+    ch.e0 = np - R + 1;
+    ch.e1 = ch.ep;
+    states_only(h, Uin, ch);
+    flux_only(h, ch);
+    update(h, ch, h->U0, Uin, Uout, stage);
+    return KFVM_OK;
+  }
+  for (int c0 = 0; c0 < np; c0 += h->chunk) {
+    const int C = std::min(h->chunk, np - c0);
+    if (needs_halo(c0, C)) continue;
+    const Chunk ch = make_chunk(h, c0, C);
+    states_and_flux(h, Uin, ch);
+    update(h, ch, h->U0, Uin, Uout, stage);
+  }
+  CK(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+  prims(h, Uin, -h->g.H, 0);
+  prims(h, Uin, np, np + h->g.H);
+  for (int c0 = 0; c0 < np; c0 += h->chunk) {
+    const int C = std::min(h->chunk, np - c0);
+    if (!needs_halo(c0, C)) continue;
+    const Chunk ch = make_chunk(h, c0, C);
     states_and_flux(h, Uin, ch);
     update(h, ch, h->U0, Uin, Uout, stage);
   }
@@ -962,6 +1056,10 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     bad(cudaMemset(h->d_smax, 0, sizeof(unsigned long long)), "memset");
   }
   bad(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
+  bad(cudaStreamCreateWithFlags(&h->s_halo, cudaStreamNonBlocking), "stream");
+  bad(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming), "event");
+  bad(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming), "event");
+  h->overlap = h->nranks > 1 ? 1 : 0;
   bad(cudaEventCreate(&h->ev[0]), "event");
   bad(cudaEventCreate(&h->ev[1]), "event");
   if (rc == KFVM_OK) rc = ensure_dt_cap(h, 1024);
@@ -998,6 +1096,9 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
                   (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_tt})
     if (p) cudaFree(p);
   if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->s_halo) cudaStreamDestroy(h->s_halo);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_halo) cudaEventDestroy(h->ev_halo);
   delete h;
 }
 
@@ -1053,7 +1154,7 @@ extern "C" int kfvm_gpu_rhs(kfvm_handle* h, double* dUdt_host) {
 }
 
 extern "C" int kfvm_gpu_states(kfvm_handle* h, double* states_host) {
-  int rc = halo(h, h->U0);
+  int rc = halo(h, h->U0, h->stream);
   if (rc) return rc;
   prims(h, h->U0);
   const long long per_cell = (long long)h->NP * h->nv;
@@ -1210,6 +1311,14 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
     } else {
       h->engine = value ? 2 : 0;
     }
+    if (h->graph) {
+      cudaGraphExecDestroy(h->graph);
+      h->graph = nullptr;
+    }
+    return KFVM_OK;
+  }
+  if (n == "overlap") {
+    h->overlap = value != 0;
     if (h->graph) {
       cudaGraphExecDestroy(h->graph);
       h->graph = nullptr;

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
   bid /= nseg;
   const int b = bid % ch.em;          // extended mid index
   const int zblk = bid / ch.em;
-  const int cstart = zblk * KZ, cend = min(ch.ep, cstart + KZ);
+  const int cstart = ch.e0 + zblk * KZ, cend = min(ch.e1, cstart + KZ);
   const int j = D == 3 ? b - 1 : 0;
   const int x0 = seg * 32 - 1;        // x of the segment's first cell
   // warp w owns the cells w, w+4, ..., w+28 of the segment (stride 4): the 4
@@ -489,8 +489,8 @@ __global__ void __launch_bounds__(128) k_limit_states(const double* __restrict__
                                                       double* __restrict__ St, Geo g, Chunk ch,
                                                       int* __restrict__ err) {
   constexpr int nv = D + 2, NP = Gen<D, R>::NP;
-  const long long tid = (long long)blockIdx.x * 128 + threadIdx.x;
-  if (tid >= ch.next) return;
+  const long long tid = (long long)ch.e0 * ch.ex * ch.em + (long long)blockIdx.x * 128 + threadIdx.x;
+  if (tid >= (long long)ch.e1 * ch.ex * ch.em) return;
   const int a = (int)(tid % ch.ex);
   const long long r1 = tid / ch.ex;
   const int b = (int)(r1 % ch.em), c = (int)(r1 / ch.em);
