@@ -204,11 +204,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", type=int, default=None,
-                    help="reconstruction kernel: 0 generic, 1 DFMA, 2 DMMA (default: per dim)")
+                    help="reconstruction kernel: 0 generic, 1 DFMA, 2 DMMA, 3 fused 2-D stage, "
+                         "4 row-marching DFMA (default: 4 in 2-D, 2 in 3-D)")
     ap.add_argument("--opt", action="append", default=[], metavar="NAME=VALUE",
                     help="extra solver option (kfvm_gpu_set_option), e.g. overlap=1")
     ap.add_argument("--kz", type=int, default=None,
-                    help="slab-axis planes marched by one reconstruction CTA (engines 2, 3)")
+                    help="slab-axis planes marched by one reconstruction CTA (engines 2-4)")
     args = ap.parse_args()
 
     import paper_2401_16543_b200 as K
@@ -347,7 +348,8 @@ def main():
                     "h2d_bytes_per_step": nloc * 8, "d2h_bytes_per_step": nloc * 8,
                     "steps": e2e_steps, "api": "Solver.set_state/ssp_rk3_step/get_state (C-ABI)"},
             "roofline": {"bound": "fp64", "kernel": "k_states_* (reconstruction+WENO-AO+limiter)",
-                         "engine": "DMMA (FP64 tensor)" if g.dim == 3 else "DFMA (unrolled)",
+                         "engine": "DMMA (FP64 tensor, plane-marching)" if g.dim == 3
+                         else "DFMA (unrolled, row-marching smem rings)",
                          "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
                          "frac": (achieved / fp64) if achieved else None,
                          "peak_source": fp64_src,

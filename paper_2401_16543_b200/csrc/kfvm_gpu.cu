@@ -518,8 +518,8 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
       // fused states + interior face fluxes, then the tile-edge faces
       const int KZ = h->kz;
       const long long nblk3 = (long long)((ch.ex + 31) / 32) * ((ch.ep + KZ - 1) / KZ);
-      k_stage_row<R><<<(unsigned)nblk3, 128, 0, h->stream>>>(U, h->Pr, h->St, h->F, h->g, ch, KZ,
-                                                             h->d_err);
+      k_stage_row<R, true><<<(unsigned)nblk3, 128, 0, h->stream>>>(U, h->Pr, h->St, h->F, h->g,
+                                                                   ch, KZ, h->d_err);
       dbg_sync(h, "k_stage_row");
       h->launches++;
       toc(h, &h->t_states);
@@ -533,6 +533,17 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
         h->launches++;
       }
       toc(h, &h->t_flux);
+      return;
+    }
+  }
+  if constexpr (DIM == 2) {
+    if (h->engine == 4) {
+      const int KZ = h->kz;
+      const long long nblk4 = (long long)((ch.ex + 31) / 32) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
+      k_stage_row<R, false><<<(unsigned)nblk4, 128, 0, h->stream>>>(U, h->Pr, h->St, h->F, h->g,
+                                                                    ch, KZ, h->d_err);
+      h->launches++;
+      toc(h, &h->t_states);
       return;
     }
   }
@@ -908,9 +919,9 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   h->R = cfg->radius;
   h->nv = cfg->dim + 2;
   h->NP = t->n_points;
-  // measured: unrolled DFMA for 2-D, tensor cores for 3-D
-  h->engine = cfg->dim == 2 ? 1 : 2;
-  h->kz = cfg->dim == 3 && cfg->radius == 3 ? 32 : 16;
+  // measured: row-marching DFMA for 2-D, tensor cores for 3-D
+  h->engine = cfg->dim == 2 ? 4 : 2;
+  h->kz = cfg->dim == 2 ? 8 : (cfg->radius == 3 ? 32 : 16);
   if (dist) {
     h->rank = dist->rank;
     h->nranks = dist->nranks;
@@ -1304,9 +1315,10 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
   std::string n(name ? name : "");
   if (n == "fast_states" || n == "engine") {
     if (n == "engine") {
-      if (value < 0 || value > 3 || (value == 3 && h->dim != 2))
+      if (value < 0 || value > 4 || (value >= 3 && h->dim != 2))
         return fail(h, KFVM_ERR_CONFIG,
-                    "engine: 0 generic, 1 DFMA, 2 tensor core, 3 DFMA row-marching (2-D)");
+                    "engine: 0 generic, 1 DFMA, 2 tensor core, 3 fused 2-D stage, "
+                    "4 row-marching DFMA (2-D)");
       h->engine = (int)value;
     } else {
       h->engine = value ? 2 : 0;

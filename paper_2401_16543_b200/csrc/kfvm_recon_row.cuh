@@ -24,8 +24,9 @@
 
 #include <cuda_pipeline.h>
 
+// resident CTAs per SM (register cap 80 / 96): measured on config 2
 #ifndef KFVM_ROW_MINB
-#define KFVM_ROW_MINB 4
+#define KFVM_ROW_MINB(R) ((R) == 2 ? 6 : 5)
 #endif
 
 template <int R>
@@ -40,8 +41,10 @@ struct RowCfg {
   static constexpr int PRING = 4;
 };
 
-template <int R>
-__global__ void __launch_bounds__(128, KFVM_ROW_MINB)
+// FUSE = false: the same row-marching reconstruction writing every face
+// state to St (k_flux follows), for comparison.
+template <int R, bool FUSE>
+__global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
     k_stage_row(const double* __restrict__ U, const double* __restrict__ Pr,
                 double* __restrict__ St, double* __restrict__ F, Geo g, Chunk ch, int KZ,
                 int* __restrict__ err) {
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB)
   const int nseg = (ch.ex + 31) >> 5;
   const int seg = blockIdx.x % nseg;
   const int zblk = blockIdx.x / nseg;
-  const int cstart = zblk * KZ, cend = min(ch.ep, cstart + KZ);
+  const int cstart = ch.e0 + zblk * KZ, cend = min(ch.e1, cstart + KZ);
   const int x0 = seg * 32 - 1;  // x of the segment's first extended cell
   const int a = seg * 32 + lane;
   const bool active = a < ch.ex;
@@ -199,6 +202,10 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB)
       const bool first = c == cstart, last = c == cend - 1;
       epilogue_core<D, NP>(err, sW, sS, sTh, T, Ubar, pr0[icn], lane, wv, active,
                            [&](int s2, int v, double u) {
+                             if (!FUSE) {
+                               St[(long long)(s2 * nv + v) * ch.next + tid] = u;
+                               return;
+                             }
                              sSt[(s2 * nv + v) * 32 + lane] = u;
                              const bool edge = (lane == 0 && s2 < RP) ||
                                                (lane == 31 && s2 >= RP && s2 < 2 * RP) ||
@@ -206,6 +213,11 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB)
                                                (last && s2 >= 3 * RP);
                              if (edge) St[(long long)(s2 * nv + v) * ch.next + tid] = u;
                            });
+    }
+    if (!FUSE) {
+      __pipeline_wait_prior(0);
+      __syncthreads();
+      continue;
     }
     __syncthreads();
     // ---- Riemann point tasks: x-faces (lane | lane+1), y-faces (row below | this row)

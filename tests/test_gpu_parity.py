@@ -134,7 +134,7 @@ def test_engines_bitwise_identical(require_gpu, idx, n):
     bit for bit."""
     g, ic, U, rset = _setup(idx, n, {})
     outs = []
-    for eng in ((0, 1, 2, 3) if g.dim == 2 else (0, 1, 2)):
+    for eng in ((0, 1, 2, 3, 4) if g.dim == 2 else (0, 1, 2)):
         with K.Solver(g, rset) as s:
             s.set_option("engine", eng)
             s.set_state(U)
