@@ -183,6 +183,18 @@ def run_reference(args, w, rset, rank):
     print(json.dumps(line), flush=True)
 
 
+def traffic_of(config_index):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/r01/roofline_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
+            t = json.load(f)[str(config_index)]
+        return (t["dram_read_bytes"] + t["dram_write_bytes"],
+                "dram read+write bytes per launch, ncu --set full: profiles/r01/" + t["capture"])
+    except Exception:
+        return None, None
+
+
 def workload_config(w, args):
     g = w.grid
     shape = "x".join(str(x) for x in ((g.nx, g.ny, g.nz) if g.dim == 3 else (g.nx, g.ny)))
@@ -354,7 +366,8 @@ def main():
                          "frac": (achieved / fp64) if achieved else None,
                          "peak_source": fp64_src,
                          "algorithmic_flops_per_cell_stage": F,
-                         "traffic": None},
+                         "traffic": traffic_of(w.index)[0],
+                         "traffic_source": traffic_of(w.index)[1]},
             "kernel_ms_per_step": kt,
             "whole_step_fp64_frac": F * value / 1e12 / fp64,
             "gpu_launches": launches,
