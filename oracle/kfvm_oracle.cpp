@@ -166,15 +166,18 @@ void weno_field(const kfvm_table* t, const Consts& k, const double* g, double* b
     for (int q = 0; q < NS; ++q) omega_out[q] = om[q];
   c[0] = om[0] * (1.0 / t->gamma_lin[0]);
   for (int q = 1; q < NS; ++q) c[q] = fma(-c[0], t->gamma_lin[q], om[q]);
+  // WENO-AO value at point s: sum_q c_q (r_qs . g_q), evaluated
+  // as ONE stencil-order fma chain over every stencil entry with the entry
+  // scaled by its stencil's coefficient first: v = fma(r_qsh, c_q * g_h, v),
+  // q = 0..NS-1, h in stencil order (this is the order in which
+  // the FP64 tensor-core engine accumulates, with no per-stencil partials).
   for (int s = 0; s < t->n_points; ++s) {
     double v = 0.0;
     for (int q = 0; q < NS; ++q) {
       const int N = t->size[q];
       const int* gat = t->gather + t->cell_offset[q];
       const double* r = t->face + (size_t)t->cell_offset[q] * t->n_points + (size_t)s * N;
-      double p = 0.0;
-      for (int h = 0; h < N; ++h) p = fma(r[h], g[gat[h]], p);
-      v = (q == 0) ? c[0] * p : fma(c[q], p, v);
+      for (int h = 0; h < N; ++h) v = fma(r[h], c[q] * g[gat[h]], v);
     }
     vals[s] = v;
   }

@@ -841,7 +841,15 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
     if (t->gather[i] != G::GATHER[i])
       return fail(h, KFVM_ERR_CONFIG, "table substencils differ from kfvm_gen.cuh");
   if constexpr (G::UNROLLED) {
-    CK(cudaMemcpyToSymbol(G::face_symbol(), t->face, sizeof(double) * G::NTOT * G::NP));
+    // face weights transposed per stencil to [q][h][s] (generated weno() order)
+    std::vector<double> ft((size_t)G::NTOT * G::NP);
+    for (int q = 0; q < G::NS; ++q) {
+      const int N = t->size[q], o = t->cell_offset[q];
+      for (int hh = 0; hh < N; ++hh)
+        for (int sp = 0; sp < G::NP; ++sp)
+          ft[(size_t)(o + hh) * G::NP + sp] = t->face[(size_t)o * G::NP + (size_t)sp * N + hh];
+    }
+    CK(cudaMemcpyToSymbol(G::face_symbol(), ft.data(), sizeof(double) * G::NTOT * G::NP));
     CK(cudaMemcpyToSymbol(G::deriv_symbol(), t->deriv, sizeof(double) * G::NTOT * G::NA));
   }
   // DMMA operands: per 4-entry chunk of each stencil (zero-padded at the

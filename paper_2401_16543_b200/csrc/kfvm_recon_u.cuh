@@ -272,20 +272,25 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
     }
     __syncwarp();
     PHASE_MARK(2);
-    // ---- pass 2: face-point columns, WENO-AO combination; point tiles in
+    // ---- pass 2: face-point columns.  The A operand of a chunk of stencil q
+    // is the transformed value scaled by the lane's cell's c_q, so ONE
+    // accumulator chain per (variable, point) runs through all stencils and
+    // ends as the WENO-AO value (oracle weno_field order).  Point tiles in
     // groups of PG (registers); with more than one group the limited states
-    // are produced by k_limit_states from the unlimited ones stored here
+    // are produced by k_limit_states from the unlimited ones stored here.
     constexpr int PG = C::PG, NG = C::NG;
     double V[nv][PG][2];
 #pragma unroll
     for (int grp = 0; grp < NG; ++grp) {
       const int t0 = grp * PG;
-      double acc[nv][PG][2];
 #pragma unroll
       for (int u = 0; u < nv; ++u)
 #pragma unroll
-        for (int n = 0; n < PG; ++n) acc[u][n][0] = acc[u][n][1] = V[u][n][0] = V[u][n][1] = 0.0;
+        for (int n = 0; n < PG; ++n) V[u][n][0] = V[u][n][1] = 0.0;
       int q = 0;
+      double cq[nv];
+#pragma unroll
+      for (int v = 0; v < nv; ++v) cq[v] = sCw[v * 8 + r8];
       // software pipeline: fragments of chunk ck+1 load while chunk ck issues
       double av[nv], bv[PG];
       {
@@ -307,34 +312,22 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
 #pragma unroll
         for (int n = 0; n < PG; ++n)
           bn[n] = t0 + n < NPT ? Bfp[(cn * NPT + t0 + n) * 32 + lane] : 0.0;
-        double aw[nv];  // W = Phi U at the slot, with this lane's cell's Phi
+        double aw[nv];  // c_q (Phi U)_v at the slot, with this lane's cell's Phi
 #pragma unroll
-        for (int v = 0; v < nv; ++v) aw[v] = phi_row<D>(T, av, v);
+        for (int v = 0; v < nv; ++v) aw[v] = cq[v] * phi_row<D>(T, av, v);
 #pragma unroll
         for (int n = 0; n < PG; ++n)
           if (t0 + n < NPT)
 #pragma unroll
-            for (int v = 0; v < nv; ++v) dmma(acc[v][n][0], acc[v][n][1], aw[v], bv[n]);
+            for (int v = 0; v < nv; ++v) dmma(V[v][n][0], V[v][n][1], aw[v], bv[n]);
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
         for (int n = 0; n < PG; ++n) bv[n] = bn[n];
-        if (sQ[ck] & 256) {
-          double cq[nv];
+        if ((sQ[ck] & 256) && q + 1 < NS) {
+          ++q;
 #pragma unroll
           for (int v = 0; v < nv; ++v) cq[v] = sCw[(q * nv + v) * 8 + r8];
-#pragma unroll
-          for (int n = 0; n < PG; ++n)
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-#pragma unroll
-              for (int v = 0; v < nv; ++v)
-                V[v][n][e] = q == 0 ? cq[v] * acc[v][n][e] : fma(cq[v], acc[v][n][e], V[v][n][e]);
-#pragma unroll
-          for (int u = 0; u < nv; ++u)
-#pragma unroll
-            for (int n = 0; n < PG; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
-          ++q;
         }
       }
       if constexpr (NG > 1) {

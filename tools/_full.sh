@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
-python bench.py > gpurun_out/bench_default.log 2>&1; tail -1 gpurun_out/bench_default.log | cut -c1-300
-python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log | cut -c1-300
-for c in 1 3; do python bench.py --config $c --steps 5 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg $c', '%.3e'%d['value'], 'e2e %.3e'%d['e2e']['value'], {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()})"; done
+for c in 2 3; do python bench.py --config $c --steps 5 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg $c', '%.3e'%d['value'], 'frac %.3f'%d['roofline']['frac'], {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()})"; done
+python bench.py --config 5 --n 256 --steps 2 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg 5@256', '%.3e'%d['value'], 'frac %.3f'%d['roofline']['frac'], {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()})"

@@ -84,7 +84,7 @@ def gen_case(dim, R):
     L.append(f"// ---- dim={dim} R={R}: N0={len(full)} sizes={sizes} n_alpha={na} n_points={npnt}")
     unrolled = (dim, R) in UNROLLED
     if unrolled:
-        L.append(f"__constant__ __align__(16) double c_f{tag}[{total * npnt}];  // table.face, [q][s][h]")
+        L.append(f"__constant__ __align__(16) double c_f{tag}[{total * npnt}];  // table.face transposed, [q][h][s]")
         L.append(f"__constant__ __align__(16) double c_d{tag}[{total * na}];  // table.deriv, [q][a][h]")
     L.append(f"template <> struct Gen<{dim}, {R}> {{")
     L.append(f"  static constexpr int N0 = {len(full)}, NP = {npnt}, NA = {na}, NS = {ns}, NTOT = {total};")
@@ -142,19 +142,20 @@ def gen_case(dim, R):
     L.append("    const double c0 = om0 * inv_g0;")
     for q in range(1, ns):
         L.append(f"    const double c{q} = fma(-c0, gam[{q}], om{q});")
+    # face points: one chain per point over every stencil entry, the entry
+    # scaled by its stencil's coefficient (oracle weno_field); c_f is the
+    # face table transposed to [q][h][s] so the point weights of one entry
+    # are adjacent (paired uniform loads)
     for s_ in range(npnt):
-        L.append("    {")
-        for q in range(ns):
-            m, N, o = members[q], sizes[q], offs[q]
-            base = o * npnt + s_ * N
-            L.append(f"      double p{q} = 0.0;")
-            for hh, h in enumerate(m):
-                L.append(f"      p{q} = fma(c_f{tag}[{base + hh}], g[{h}], p{q});")
-        L.append("      double v = c0 * p0;")
-        for q in range(1, ns):
-            L.append(f"      v = fma(c{q}, p{q}, v);")
-        L.append(f"      w[{s_}] = v;")
-        L.append("    }")
+        L.append(f"    w[{s_}] = 0.0;")
+    for q in range(ns):
+        m, N, o = members[q], sizes[q], offs[q]
+        for hh, h in enumerate(m):
+            L.append("    {")
+            L.append(f"      const double cg = c{q} * g[{h}];")
+            for s_ in range(npnt):
+                L.append(f"      w[{s_}] = fma(c_f{tag}[{(o + hh) * npnt + s_}], cg, w[{s_}]);")
+            L.append("    }")
     L.append("  }")
     L.append("};")
     return "\n".join(L)
