@@ -106,6 +106,11 @@ typedef struct kfvm_config {
   double eps;         /* WENO epsilon, 1e-40 */
   double kappa;       /* positivity bound relaxation, 0.4 */
   double flattener_kf;/* flattener kappa_f, 0.33 */
+  int kxrcf;          /* KXRCF troubled-cell indicator (
+                         config key kxrcf.enabled): 0 = WENO in every
+                         cell (default), 1 = unlimited full-stencil states with
+                         WENO only in flagged cells */
+  double kxrcf_m;     /* the indicator's power m on Delta (kxrcf.m), 1.5 */
 } kfvm_config;
 
 /* Fill cfg with the reference defaults for the given geometry. */
@@ -168,6 +173,11 @@ int kfvm_gpu_get_state(kfvm_handle* h, double* U_host);
 /* Same on device memory (AoS, caller-owned device pointer). */
 int kfvm_gpu_set_state_device(kfvm_handle* h, const double* U_dev);
 int kfvm_gpu_get_state_device(kfvm_handle* h, double* U_dev);
+
+/* KXRCF troubled-cell flags (1 = WENO) of the rank's cells for the current
+ * state, AoS cell order; replaces kxrcf_flag on the path.  Requires a
+ * handle created with cfg->kxrcf = 1. */
+int kfvm_gpu_kxrcf_flags(kfvm_handle* h, unsigned char* flags_host);
 
 /* One compute_rhs: dU/dt of the current state (AoS host). */
 int kfvm_gpu_rhs(kfvm_handle* h, double* dUdt_host);

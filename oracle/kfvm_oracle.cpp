@@ -12,6 +12,7 @@
 //   flattener, bounds, density/pressure limit .. S:410-446
 //   Roe/Batten speeds, HLL, HLLC ............... S:477-503
 //   fill_ghost (periodic/outflow) .............. S:553-561 (outflow = index clamp)
+//   KXRCF pass 1 / flags / flagged-only WENO ...... S:401-409
 //   reconstruct_states (KXRCF off) ............. S:562-570
 //   compute_rhs ................................ S:589-597
 //   SSP-RK3 (BASELINE.json; replaces S:598) .... Shu-Osher form
@@ -35,6 +36,8 @@ struct Consts {
   int n[3];
   double gamma, gm1, inv_gm1, dx, cfl, eps, kappa, kf, onepk, onemk;
   double scale[32];  // Delta^(2|alpha|)
+  int kx;            // KXRCF on
+  double dm;         // Delta^m (host std::pow, the same double the GPU handle uses)
 };
 
 Consts make_consts(const kfvm_config* c, const kfvm_table* t) {
@@ -57,6 +60,8 @@ Consts make_consts(const kfvm_config* c, const kfvm_table* t) {
   k.kf = c->flattener_kf;
   k.onepk = 1.0 + c->kappa;
   k.onemk = 1.0 - c->kappa;
+  k.kx = c->kxrcf;
+  k.dm = std::pow(c->dx, c->kxrcf_m);
   if (t) {
     for (int a = 0; a < t->n_alpha; ++a) {
       const int ord = t->alpha[3 * a] + t->alpha[3 * a + 1] + t->alpha[3 * a + 2];
@@ -425,6 +430,148 @@ void parallel_for(int n, int nthreads, F&& f) {
   for (auto& x : th) x.join();
 }
 
+size_t ncells(const Consts& k);
+
+// ------------------------------------------------------------------ KXRCF
+// Troubled-cell indicator: entropy q = p / rho^gamma.
+// rho^gamma is evaluated with a pinned exp/log built from IEEE +,*,fma, rint
+// and exponent bit manipulation only (no libm), so the CPU and the GPU get
+// the same bits; the result only feeds the threshold test.
+inline double kf_log(double x) {  // x > 0, finite, normal
+  uint64_t b;
+  std::memcpy(&b, &x, 8);
+  int e = (int)((b >> 52) & 0x7ff) - 1023;
+  b = (b & 0x000fffffffffffffULL) | 0x3ff0000000000000ULL;
+  double m;
+  std::memcpy(&m, &b, 8);  // [1, 2)
+  if (m > 0x1.6a09e667f3bcdp+0) {  // sqrt(2)
+    m = m * 0.5;
+    e += 1;
+  }
+  const double f = m - 1.0;
+  const double sv = f / (2.0 + f);
+  const double z = sv * sv;
+  // log m = 2 atanh(s) = 2 s sum_k z^k / (2k+1), k = 0..9
+  double P = 0x1.af286bca1af28p-5;  // 1/19
+  P = fma(P, z, 0x1.e1e1e1e1e1e1ep-5);
+  P = fma(P, z, 0x1.1111111111111p-4);
+  P = fma(P, z, 0x1.3b13b13b13b14p-4);
+  P = fma(P, z, 0x1.745d1745d1746p-4);
+  P = fma(P, z, 0x1.c71c71c71c71cp-4);
+  P = fma(P, z, 0x1.2492492492492p-3);
+  P = fma(P, z, 0x1.999999999999ap-3);
+  P = fma(P, z, 0x1.5555555555555p-2);
+  P = fma(P, z, 1.0);
+  const double lm = (2.0 * sv) * P;
+  const double de = (double)e;
+  return fma(de, 0x1.62e4200000000p-1, fma(de, 0x1.fdf473de6af28p-22, lm));
+}
+inline double kf_exp(double y) {  // |y| < 700
+  const double n = std::rint(y * 0x1.71547652b82fep+0);
+  double r = fma(-n, 0x1.62e4200000000p-1, y);
+  r = fma(-n, 0x1.fdf473de6af28p-22, r);
+  double p = 0x1.6124613a86d09p-33;  // 1/13!
+  p = fma(p, r, 0x1.1eed8eff8d898p-29);
+  p = fma(p, r, 0x1.ae64567f544e4p-26);
+  p = fma(p, r, 0x1.27e4fb7789f5cp-22);
+  p = fma(p, r, 0x1.71de3a556c734p-19);
+  p = fma(p, r, 0x1.a01a01a01a01ap-16);
+  p = fma(p, r, 0x1.a01a01a01a01ap-13);
+  p = fma(p, r, 0x1.6c16c16c16c17p-10);
+  p = fma(p, r, 0x1.1111111111111p-7);
+  p = fma(p, r, 0x1.5555555555555p-5);
+  p = fma(p, r, 0x1.5555555555555p-3);
+  p = fma(p, r, 0x1.0000000000000p-1);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  return std::ldexp(p, (int)n);
+}
+inline double kf_pow(double x, double y) { return kf_exp(y * kf_log(x)); }
+
+// entropy p / rho^gamma of a pointwise state; NaN for rho <= 0 (flags the cell)
+inline double entropy(const Consts& k, const double* U) {
+  if (!(U[0] > 0.0)) return NAN;
+  return pressure(k.dim, U, k.gm1) / kf_pow(U[0], k.gamma);
+}
+
+// Unlimited full-stencil states (pass 1): conservative variables,
+// r_0 vectors, stencil-order fma chains.
+void pass1_cell(const kfvm_table* t, const Consts& k, const Slab& S, int i, int j, int kk,
+                double* st) {
+  const int nv = k.nv, N0 = t->n_full, np = t->n_points;
+  for (int s = 0; s < np; ++s) {
+    const double* r = t->face + (size_t)s * N0;  // stencil 0 is first in the table
+    for (int v = 0; v < nv; ++v) {
+      double acc = 0.0;
+      for (int h = 0; h < N0; ++h)
+        acc = fma(r[h], S.at(i + t->offsets[3 * h], j + t->offsets[3 * h + 1],
+                             kk + t->offsets[3 * h + 2])[v],
+                  acc);
+      st[s * nv + v] = acc;
+    }
+  }
+}
+
+// Flags of every global cell (pass 2): flagged iff
+// max_s |q_s(+) - q_s(-)| / <Q> >= Delta^m, <Q> = p(Ubar) / rhobar^gamma, over
+// the points of every face with a neighbour (physical-boundary faces of
+// outflow domains are exempt); a NaN jump or <Q> flags the cell.
+std::vector<uint8_t> global_flags(const kfvm_table* t, const Consts& k, const double* U,
+                                  int nthreads) {
+  const int dim = k.dim, nv = k.nv, np = t->n_points, rp = np / (2 * dim);
+  Slab S;
+  S.init(k, 0, k.n[dim - 1]);
+  S.load(U);
+  const size_t nc = ncells(k), cs = (size_t)np * nv;
+  std::vector<double> st(nc * cs);
+  const int nrows = k.n[1] * k.n[2];
+  parallel_for(nrows, nthreads, [&](int row) {
+    const int j = row % k.n[1], kk = row / k.n[1];
+    for (int i = 0; i < k.n[0]; ++i)
+      pass1_cell(t, k, S, i, j, kk, st.data() + (((size_t)kk * k.n[1] + j) * k.n[0] + i) * cs);
+  });
+  std::vector<uint8_t> fl(nc, 0);
+  parallel_for(nrows, nthreads, [&](int row) {
+    const int j = row % k.n[1], kk = row / k.n[1];
+    for (int i = 0; i < k.n[0]; ++i) {
+      const int c[3] = {i, j, kk};
+      const size_t id = ((size_t)kk * k.n[1] + j) * k.n[0] + i;
+      const double* Uc = U + id * nv;
+      const double Q = Uc[0] > 0.0 ? pressure(dim, Uc, k.gm1) / kf_pow(Uc[0], k.gamma) : NAN;
+      double jmax = 0.0;
+      bool nan = !(Q == Q);
+      for (int d = 0; d < dim; ++d)
+        for (int side = 0; side < 2; ++side) {
+          int nb[3] = {c[0], c[1], c[2]};
+          nb[d] += side ? 1 : -1;
+          if (nb[d] < 0 || nb[d] >= k.n[d]) {
+            if (k.bc != KFVM_BC_PERIODIC) continue;  // physical boundary face: exempt
+            nb[d] = (nb[d] + k.n[d]) % k.n[d];
+          }
+          const size_t nid = ((size_t)nb[2] * k.n[1] + nb[1]) * k.n[0] + nb[0];
+          for (int m = 0; m < rp; ++m) {
+            const int so = (2 * d + side) * rp + m, sn = (2 * d + 1 - side) * rp + m;
+            const double jq = std::fabs(entropy(k, st.data() + nid * cs + sn * nv) -
+                                        entropy(k, st.data() + id * cs + so * nv));
+            if (!(jq == jq)) nan = true;
+            jmax = std::fmax(jmax, jq);
+          }
+        }
+      fl[id] = (nan || jmax / Q >= k.dm) ? 1 : 0;
+    }
+  });
+  return fl;
+}
+
+// flag of any cell of an extended box: global cells are their own, ghost
+// cells take the flag of the cell they replicate (periodic image / outflow
+// clamp)
+inline int flag_of(const Consts& k, const uint8_t* fl, int i, int j, int kk) {
+  const int c[3] = {wrap(i, k.n[0], k.bc), wrap(j, k.n[1], k.bc),
+                    k.dim == 3 ? wrap(kk, k.n[2], k.bc) : 0};
+  return fl[((size_t)c[2] * k.n[1] + c[1]) * k.n[0] + c[0]];
+}
+
 // Face states of one cell (global coords), after WENO-AO + positivity.
 int cell_states(const kfvm_table* t, const Consts& k, const Slab& S, int i, int j, int kk,
                 double* st /* [npts][nv] */) {
@@ -451,9 +598,25 @@ int cell_states(const kfvm_table* t, const Consts& k, const Slab& S, int i, int 
   return limit_cell(k, np, st, nbr, nullptr);
 }
 
+// KXRCF face states of one cell: WENO-AO (cell_states) when flagged, else the
+// pass-1 states; positivity limiting in both cases.
+int cell_states_kx(const kfvm_table* t, const Consts& k, const Slab& S, const uint8_t* fl,
+                   int i, int j, int kk, double* st) {
+  if (flag_of(k, fl, i, j, kk)) return cell_states(t, k, S, i, j, kk, st);
+  const int dim = k.dim, nv = k.nv;
+  pass1_cell(t, k, S, i, j, kk, st);
+  double nbr[27 * 5];
+  const int kr = dim == 3 ? 1 : 0;
+  int m = 0;
+  for (int c = -kr; c <= kr; ++c)
+    for (int b = -1; b <= 1; ++b)
+      for (int a = -1; a <= 1; ++a, ++m) std::memcpy(nbr + m * nv, S.at(i + a, j + b, kk + c), nv * sizeof(double));
+  return limit_cell(k, t->n_points, st, nbr, nullptr);
+}
+
 // RHS over the slab's interior planes.  out: AoS [np planes]
 int slab_rhs(const kfvm_table* t, const Consts& k, const Slab& S, double* out, int nthreads,
-             double* states_out = nullptr) {
+             double* states_out = nullptr, const uint8_t* flags = nullptr) {
   const int dim = k.dim, nv = k.nv, npts = t->n_points;
   const int rp = npts / (2 * dim);
   // extended-cell box: [-1, n] in every axis, slab axis [p0-1, p0+np]
@@ -479,7 +642,9 @@ int slab_rhs(const kfvm_table* t, const Consts& k, const Slab& S, double* out, i
     const int b = row % cnt[1], c = row / cnt[1];
     for (int a = 0; a < cnt[0]; ++a) {
       const size_t id = ((size_t)c * cnt[1] + b) * cnt[0] + a;
-      const int e = cell_states(t, k, S, lo[0] + a, lo[1] + b, lo[2] + c, st.data() + id * cs);
+      const int e = flags ? cell_states_kx(t, k, S, flags, lo[0] + a, lo[1] + b, lo[2] + c,
+                                           st.data() + id * cs)
+                          : cell_states(t, k, S, lo[0] + a, lo[1] + b, lo[2] + c, st.data() + id * cs);
       if (e) err.store(e);
     }
   });
@@ -571,13 +736,16 @@ int full_rhs(const kfvm_table* t, const Consts& k, const double* U, double* out,
              int nthreads) {
   const int sa = k.dim - 1;
   const size_t plane = ncells(k) / k.n[sa] * k.nv;
+  std::vector<uint8_t> fl;
+  if (k.kx) fl = global_flags(t, k, U, nthreads);
   for (int r = 0; r < nslabs; ++r) {
     int p0, np;
     slab_range(k.n[sa], nslabs, r, &p0, &np);
     Slab S;
     S.init(k, p0, np);
     S.load(U);
-    const int e = slab_rhs(t, k, S, out + (size_t)p0 * plane, nthreads);
+    const int e = slab_rhs(t, k, S, out + (size_t)p0 * plane, nthreads, nullptr,
+                           k.kx ? fl.data() : nullptr);
     if (e) return e;
   }
   return 0;
@@ -600,8 +768,21 @@ int kfo_states(const kfvm_config* cfg, const kfvm_table* t, const double* U, dou
   S.init(k, 0, k.n[k.dim - 1]);
   S.load(U);
   std::vector<double> tmp(ncells(k) * k.nv);
-  return slab_rhs(t, k, S, tmp.data(), nthreads, states);
+  std::vector<uint8_t> fl;
+  if (k.kx) fl = global_flags(t, k, U, nthreads);
+  return slab_rhs(t, k, S, tmp.data(), nthreads, states, k.kx ? fl.data() : nullptr);
 }
+
+// KXRCF flags of every cell (1 = WENO), global AoS cell order
+int kfo_kxrcf_flags(const kfvm_config* cfg, const kfvm_table* t, const double* U,
+                    unsigned char* flags, int nthreads) {
+  const Consts k = make_consts(cfg, t);
+  const std::vector<uint8_t> fl = global_flags(t, k, U, nthreads);
+  std::memcpy(flags, fl.data(), fl.size());
+  return 0;
+}
+
+double kfo_pow(double x, double y) { return kf_pow(x, y); }
 
 int kfo_select_dt(const kfvm_config* cfg, const double* U, double* dt) {
   const Consts k = make_consts(cfg, nullptr);

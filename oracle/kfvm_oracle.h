@@ -39,6 +39,12 @@ int kfo_run(const kfvm_config* cfg, const kfvm_table* t, double* U, int nsteps,
 int kfo_sample_stage(const kfvm_config* cfg, const kfvm_table* t, const double* U,
                      int p0, int np, int nthreads, double* seconds);
 
+/* KXRCF troubled-cell flags (1 = WENO) of every cell, and the
+ * pinned power function the indicator uses (q = p / rho^gamma). */
+int kfo_kxrcf_flags(const kfvm_config* cfg, const kfvm_table* t, const double* U,
+                    unsigned char* flags, int nthreads);
+double kfo_pow(double x, double y);
+
 /* Slab pieces for the multi-process decomposition test. */
 int kfo_slab_rhs(const kfvm_config* cfg, const kfvm_table* t, int p0, int np,
                  const double* U_local, double* out, int nthreads);

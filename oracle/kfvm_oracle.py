@@ -48,6 +48,8 @@ def lib():
             "kfo_exact_flux": (None, [I, I, P, C.c_double, P]),
             "kfo_weno": (None, [T, C.c_double, C.c_double, P, P, P, P]),
             "kfo_limit": (I, [I, I, P, P, C.c_double, C.c_double, C.c_double, P]),
+            "kfo_kxrcf_flags": (I, [CF, T, P, P, I]),
+            "kfo_pow": (C.c_double, [C.c_double, C.c_double]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -86,6 +88,14 @@ class Oracle:
         out = np.empty((n, self.rset.n_face_points(), self.grid.nvar))
         self._chk(self.L.kfo_states(C.byref(self.cfg), self.rset.c_table, _p(U), _p(out),
                                     self.nthreads), "states")
+        return out
+
+    def kxrcf_flags(self, U):
+        """KXRCF flags (1 = WENO) of every cell, shape of the grid."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.zeros(self.grid.shape, dtype=np.uint8)
+        self._chk(self.L.kfo_kxrcf_flags(C.byref(self.cfg), self.rset.c_table, _p(U), _p(out),
+                                         self.nthreads), "kxrcf_flags")
         return out
 
     def select_dt(self, U):

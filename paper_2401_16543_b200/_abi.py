@@ -40,6 +40,7 @@ class KfvmConfig(C.Structure):
         ("nz", C.c_int), ("bc", C.c_int), ("riemann", C.c_int),
         ("dx", C.c_double), ("gamma", C.c_double), ("cfl", C.c_double),
         ("eps", C.c_double), ("kappa", C.c_double), ("flattener_kf", C.c_double),
+        ("kxrcf", C.c_int), ("kxrcf_m", C.c_double),
     ]
 
 
@@ -75,6 +76,7 @@ EXPORTS = [
     ("kfvm_gpu_rhs", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kfvm_gpu_states", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kfvm_gpu_select_dt", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    ("kfvm_gpu_kxrcf_flags", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kfvm_gpu_stage", C.c_int, [C.c_void_p, C.c_int, C.c_double]),
     ("kfvm_gpu_step", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("kfvm_gpu_run", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),

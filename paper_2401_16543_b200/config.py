@@ -33,6 +33,8 @@ class GridConfig:
     kappa: float = 0.4          # limiter.kappa
     flattener_kf: float = 0.33  # limiter.flattener_kf
     ell_over_delta: float = 5.0
+    kxrcf: bool = False         # kxrcf.enabled: WENO only in flagged cells
+    kxrcf_m: float = 1.5        # kxrcf.m
 
     def __post_init__(self):
         if self.dim not in (2, 3):
@@ -71,6 +73,7 @@ class GridConfig:
         c.dx = float(self.dx if self.dx is not None else 1.0 / self.nx)
         c.gamma, c.cfl, c.eps = self.gamma, self.cfl, self.eps
         c.kappa, c.flattener_kf = self.kappa, self.flattener_kf
+        c.kxrcf, c.kxrcf_m = int(bool(self.kxrcf)), float(self.kxrcf_m)
         return c
 
 

@@ -84,6 +84,7 @@ constexpr int npoints(int dim, int R) { return dim == 2 ? 4 * R : 6 * R * R; }
 #include "kfvm_recon.cuh"
 #include "kfvm_recon_u.cuh"
 #include "kfvm_recon_row.cuh"
+#include "kfvm_kxrcf.cuh"
 
 // ------------------------------------------------------------------ k_flux
 template <int DIM>
@@ -406,6 +407,7 @@ NcclApi& nccl() {
            api.GroupStart && api.GroupEnd && api.CommDestroy;
   return api;
 }
+const int kNcclUint8 = 1;   // ncclUint8
 const int kNcclUint64 = 5;  // ncclUint64
 const int kNcclDouble = 8;  // ncclFloat64
 const int kNcclMax = 2;     // ncclMax
@@ -448,6 +450,8 @@ struct kfvm_handle {
   long long launches = 0;
   long long graph_launches = 0;
   long long st_budget = 16LL << 30;
+  bool kx = false;                    // KXRCF two-pass reconstruction
+  unsigned char* d_flags = nullptr;   // KXRCF flags of the extended box
   std::string err;
 };
 
@@ -513,6 +517,35 @@ void dbg_sync(kfvm_handle* h, const char* what) {
 template <int DIM, int R>
 void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   tic(h);
+  const unsigned char* kfl = h->kx ? h->d_flags : nullptr;
+  if (kfl) {  // KXRCF: flagged cells only, unlimited states (engines 4, 2, 0)
+    const int eng = DIM == 2 ? (h->engine == 0 ? 0 : 4) : (h->engine == 0 ? 0 : 2);
+    if constexpr (DIM == 2) {
+      if (eng == 4) {
+        const int KZ = h->kz;
+        const long long nb = (long long)((ch.ex + 31) / 32) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
+        k_stage_row<R, false, true><<<(unsigned)nb, 128, 0, h->stream>>>(
+            U, h->Pr, h->St, h->F, h->g, ch, KZ, h->d_err, kfl);
+      }
+    } else {
+      if (eng == 2) {
+        const int KZ = h->kz;
+        const long long nb =
+            (long long)((ch.ex + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
+        k_states_u<DIM, R><<<(unsigned)nb, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
+            U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, kfl);
+      }
+    }
+    if (eng == 0)
+      k_states<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g,
+                                                                          ch, h->d_err, kfl);
+    h->launches++;
+    k_limit_states<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->Pr, h->St,
+                                                                            h->g, ch, h->d_err);
+    h->launches++;
+    toc(h, &h->t_states);
+    return;
+  }
   if constexpr (DIM == 2) {
     if (h->engine == 3) {
       // fused states + interior face fluxes, then the tile-edge faces
@@ -595,7 +628,7 @@ void states_only(kfvm_handle* h, const double* U, const Chunk& ch) {
   if (h->dim == 3 && h->R == 3) launch_states<3, 3>(h, U, ch);
 }
 
-bool fused_engine(const kfvm_handle* h) { return h->dim == 2 && h->engine == 3; }
+bool fused_engine(const kfvm_handle* h) { return h->dim == 2 && h->engine == 3 && !h->kx; }
 
 void flux_only(kfvm_handle* h, const Chunk& ch) {
   if (fused_engine(h)) return;
@@ -706,8 +739,54 @@ void run_planes(kfvm_handle* h, const double* Uin, double* Uout, int stage, int 
 // [R+1, np-R+1); then the halo planes' per-cell quantities and the rest.
 // Each state is still computed exactly once with unchanged arithmetic, so the
 // results are bit-identical to the serial schedule.
+// KXRCF passes 1-2: unlimited states, flags of the slab's cells,
+// the neighbouring ranks' edge-plane flags, the ghost cells' flags.
+template <int DIM, int R>
+int kx_flags(kfvm_handle* h, const double* U, const Chunk& ch) {
+  tic(h);
+  k_pass1<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->St, h->g, ch,
+                                                                     h->d_face);
+  k_kx_flag<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->d_flags,
+                                                                 h->g, ch, h->p0, h->nsa);
+  h->launches += 2;
+  if (h->nranks > 1) {
+    NcclApi& N = nccl();
+    const bool periodic = h->cfg.bc == KFVM_BC_PERIODIC;
+    const int lo = h->rank - 1, hi = h->rank + 1;
+    const bool has_lo = periodic || lo >= 0, has_hi = periodic || hi < h->nranks;
+    const int plo = (lo + h->nranks) % h->nranks, phi = hi % h->nranks;
+    const long long pl = (long long)ch.ex * ch.em;
+    unsigned char* f = h->d_flags;
+    N.GroupStart();
+    if (has_hi) N.Send(f + (long long)ch.C * pl, pl, kNcclUint8, phi, h->comm, h->stream);
+    if (has_lo) N.Recv(f, pl, kNcclUint8, plo, h->comm, h->stream);
+    if (has_lo) N.Send(f + pl, pl, kNcclUint8, plo, h->comm, h->stream);
+    if (has_hi) N.Recv(f + (long long)(ch.C + 1) * pl, pl, kNcclUint8, phi, h->comm, h->stream);
+    if (N.GroupEnd() != 0) return fail(h, KFVM_ERR_DEVICE, "ncclGroupEnd failed (flags)");
+  }
+  k_kx_mirror<DIM><<<blocks(ch.next, 256), 256, 0, h->stream>>>(h->d_flags, h->g, ch, h->p0,
+                                                                h->nsa, h->nranks);
+  h->launches++;
+  toc(h, &h->t_other);
+  return KFVM_OK;
+}
+
 int run_stage(kfvm_handle* h, const double* Uin, double* Uout, int stage) {
   const int np = h->g.np_loc, R = h->R;
+  if (h->kx) {  // single chunk (checked at create)
+    int rc = halo(h, const_cast<double*>(Uin), h->stream);
+    if (rc) return rc;
+    prims(h, Uin);
+    const Chunk ch = make_chunk(h, 0, np);
+    if (h->dim == 2 && R == 2) rc = kx_flags<2, 2>(h, Uin, ch);
+    if (h->dim == 2 && R == 3) rc = kx_flags<2, 3>(h, Uin, ch);
+    if (h->dim == 3 && R == 2) rc = kx_flags<3, 2>(h, Uin, ch);
+    if (h->dim == 3 && R == 3) rc = kx_flags<3, 3>(h, Uin, ch);
+    if (rc) return rc;
+    states_and_flux(h, Uin, ch);
+    update(h, ch, h->U0, Uin, Uout, stage);
+    return KFVM_OK;
+  }
   const int nch = (np + h->chunk - 1) / h->chunk;
   auto needs_halo = [&](int c0, int C) { return c0 - 1 - R < 0 || c0 + C + R > np - 1; };
   if (!h->overlap || fused_engine(h) || np < 2 * R + 3) {
@@ -979,6 +1058,9 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   k.onemk = 1.0 - cfg->kappa;
   k.c13 = 1.0 / 3.0;
   k.c23 = 2.0 / 3.0;
+  k.kx = cfg->kxrcf ? 1 : 0;
+  k.dm = std::pow(cfg->dx, cfg->kxrcf_m);  // the oracle computes the same std::pow
+  h->kx = cfg->kxrcf != 0;
   DevTable& T = h->tab;
   T.n_full = t->n_full;
   T.n_points = t->n_points;
@@ -1052,6 +1134,15 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     long long c = h->st_budget / per_plane - 2;
     c = std::max(1LL, std::min(c, (long long)np));
     h->chunk = (int)c;
+    if (h->kx && h->chunk < np) {
+      // the flags of a chunk's edge planes need the pass-1 states beyond them
+      rc = KFVM_ERR_CONFIG;
+      h->err = "kxrcf: the slab's face states must fit one chunk (16 GB scratch)";
+    }
+  }
+  if (h->kx && rc == KFVM_OK) {
+    const Chunk ch = make_chunk(h, 0, h->chunk);
+    bad(cudaMalloc(&h->d_flags, (size_t)ch.next), "cudaMalloc flags");
   }
   {
     const Chunk ch = make_chunk(h, 0, h->chunk);
@@ -1112,7 +1203,8 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
   for (void* p : {(void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
                   (void*)h->aos, (void*)h->d_face, (void*)h->d_deriv, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
-                  (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_tt})
+                  (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_tt,
+                  (void*)h->d_flags})
     if (p) cudaFree(p);
   if (h->stream) cudaStreamDestroy(h->stream);
   if (h->s_halo) cudaStreamDestroy(h->s_halo);
@@ -1195,6 +1287,42 @@ extern "C" int kfvm_gpu_states(kfvm_handle* h, double* states_host) {
   cudaStreamSynchronize(h->stream);
   cudaFree(dbuf);
   return check_err(h);
+}
+
+// KXRCF flags (1 = WENO) of the rank's cells for the current state, AoS order
+// (the indicator pass of kfvm_gpu_states / the stage, S:565 steps 1-2).
+__global__ void k_extract_flags(const unsigned char* __restrict__ fl, unsigned char* __restrict__ out,
+                                Geo g, Chunk ch) {
+  const long long t = (long long)blockIdx.x * 256 + threadIdx.x;
+  const long long n = (long long)g.nx * g.nm * ch.C;
+  if (t >= n) return;
+  const int x = (int)(t % g.nx);
+  const long long r = t / g.nx;
+  const int j = (int)(r % g.nm), p = (int)(r / g.nm);
+  const bool d3 = ch.em > 1;
+  out[t] = fl[((long long)(p + 1) * ch.em + (d3 ? j + 1 : 0)) * ch.ex + (x + 1)];
+}
+
+extern "C" int kfvm_gpu_kxrcf_flags(kfvm_handle* h, unsigned char* flags_host) {
+  if (!h->kx) return fail(h, KFVM_ERR_CONFIG, "kxrcf is off in this handle's config");
+  int rc = halo(h, h->U0, h->stream);
+  if (rc) return rc;
+  prims(h, h->U0);
+  const Chunk ch = make_chunk(h, 0, h->g.np_loc);
+  if (h->dim == 2 && h->R == 2) rc = kx_flags<2, 2>(h, h->U0, ch);
+  if (h->dim == 2 && h->R == 3) rc = kx_flags<2, 3>(h, h->U0, ch);
+  if (h->dim == 3 && h->R == 2) rc = kx_flags<3, 2>(h, h->U0, ch);
+  if (h->dim == 3 && h->R == 3) rc = kx_flags<3, 3>(h, h->U0, ch);
+  if (rc) return rc;
+  const long long n = (long long)h->g.nx * h->g.nm * ch.C;
+  unsigned char* d = nullptr;
+  CK(cudaMalloc(&d, (size_t)n));
+  k_extract_flags<<<blocks(n, 256), 256, 0, h->stream>>>(h->d_flags, d, h->g, ch);
+  h->launches++;
+  CK(cudaMemcpyAsync(flags_host, d, (size_t)n, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFree(d);
+  return KFVM_OK;
 }
 
 extern "C" int kfvm_gpu_select_dt(kfvm_handle* h, double* dt) {

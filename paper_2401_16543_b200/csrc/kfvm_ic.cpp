@@ -263,6 +263,8 @@ extern "C" void kfvm_config_defaults(kfvm_config* c, int dim, int radius, int nx
   c->eps = 1e-40;
   c->kappa = 0.4;
   c->flattener_kf = 0.33;
+  c->kxrcf = 0;
+  c->kxrcf_m = 1.5;
 }
 
 extern "C" void kfvm_slab_range(int n_global, int nranks, int rank, int* p0, int* np) {

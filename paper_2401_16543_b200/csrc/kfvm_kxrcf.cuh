@@ -1,0 +1,134 @@
+// kfvm_kxrcf.cuh — the KXRCF two-pass reconstruction (
+// P:343-357, §5.3 steps 1-3): unlimited full-stencil states in conservative
+// variables for every extended cell (pass 1), the troubled-cell flags from
+// the entropy jumps across the faces (pass 2), then the WENO engines run in
+// flagged cells only (their tiles are skipped otherwise) and k_limit_states
+// applies the positivity limiter to every cell.  Same operations as the
+// oracle's pass1_cell / global_flags / flag_of.
+// Included inside namespace kfvm_b200 by kfvm_gpu.cu.
+#ifndef KFVM_KXRCF_CUH_
+#define KFVM_KXRCF_CUH_
+
+// Pass 1: St[s][v][cell] = r_0(s) . U_v over S_0, stencil-order fma chains.
+template <int D, int R>
+__global__ void __launch_bounds__(128) k_pass1(const double* __restrict__ U,
+                                               double* __restrict__ St, Geo g, Chunk ch,
+                                               const double* __restrict__ face) {
+  constexpr int nv = D + 2, NP = npoints(D, R), N0 = full_size(D, R);
+  constexpr int HB = N0 < 40 ? N0 : 32;  // stencil values held per block
+  const long long tid = (long long)ch.e0 * ch.ex * ch.em + (long long)blockIdx.x * 128 + threadIdx.x;
+  if (tid >= (long long)ch.e1 * ch.ex * ch.em) return;
+  const int a = (int)(tid % ch.ex);
+  const long long r1 = tid / ch.ex;
+  const int b = (int)(r1 % ch.em), c = (int)(r1 / ch.em);
+  const int x = a - 1, j = D == 3 ? b - 1 : 0, p = ch.c0 - 1 + c;
+  for (int v = 0; v < nv; ++v) {
+    double acc[NP];
+#pragma unroll
+    for (int s = 0; s < NP; ++s) acc[s] = 0.0;
+    for (int h0 = 0; h0 < N0; h0 += HB) {
+      double u[HB];
+#pragma unroll
+      for (int hh = 0; hh < HB; ++hh) {
+        const int h = h0 + hh;
+        u[hh] = h < N0 ? __ldg(U + v * g.vstride +
+                               uidx<D>(g, x + c_t.off_x[h], j + c_t.off_m[h], p + c_t.off_p[h]))
+                       : 0.0;
+      }
+#pragma unroll
+      for (int s = 0; s < NP; ++s)
+#pragma unroll
+        for (int hh = 0; hh < HB; ++hh)
+          if (h0 + hh < N0) acc[s] = fma(__ldg(face + s * N0 + h0 + hh), u[hh], acc[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < NP; ++s) St[(long long)(s * nv + v) * ch.next + tid] = acc[s];
+  }
+}
+
+// Pass 2: flags of the slab's own cells (extended planes 1..C of the single
+// chunk).  Physical-boundary faces of outflow domains are exempt; a
+// NaN jump or cell entropy flags the cell.  p0g / nsa: the slab's first
+// global plane and the global slab-axis extent.
+template <int D, int R>
+__global__ void __launch_bounds__(128) k_kx_flag(const double* __restrict__ U,
+                                                 const double* __restrict__ Pr,
+                                                 const double* __restrict__ St,
+                                                 unsigned char* __restrict__ fl, Geo g, Chunk ch,
+                                                 int p0g, int nsa) {
+  constexpr int nv = D + 2, NP = npoints(D, R), RP = NP / (2 * D);
+  const long long tid = (long long)blockIdx.x * 128 + threadIdx.x;
+  if (tid >= ch.next) return;
+  const int a = (int)(tid % ch.ex);
+  const long long r1 = tid / ch.ex;
+  const int b = (int)(r1 % ch.em), c = (int)(r1 / ch.em);
+  const int x = a - 1, j = D == 3 ? b - 1 : 0, p = ch.c0 - 1 + c;
+  if (x < 0 || x >= g.nx || (D == 3 && (j < 0 || j >= g.nm)) || c < 1 || c > ch.C) return;
+  const long long ic = uidx<D>(g, x, j, p);
+  const double rho = __ldg(U + ic);
+  const double Q = rho > 0.0 ? __ldg(Pr + ic) / d_kf_pow(rho, c_k.gamma)
+                             : __longlong_as_double(0x7ff8000000000000LL);
+  bool nan = !(Q == Q);
+  double jmax = 0.0;
+  const bool periodic = c_k.bc == KFVM_BC_PERIODIC;
+  const int pg = p0g + p;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int coord = d == 0 ? x : (d == D - 1 ? pg : j);
+      const int n = d == 0 ? g.nx : (d == D - 1 ? nsa : g.nm);
+      if (!periodic && ((side == 0 && coord == 0) || (side == 1 && coord == n - 1))) continue;
+      const long long step = d == 0 ? 1 : (d == D - 1 ? (long long)ch.ex * ch.em : ch.ex);
+      const long long nt = side ? tid + step : tid - step;
+#pragma unroll
+      for (int m = 0; m < RP; ++m) {
+        const int so = (2 * d + side) * RP + m, sn = (2 * d + 1 - side) * RP + m;
+        double uo[nv], un[nv];
+#pragma unroll
+        for (int v = 0; v < nv; ++v) {
+          uo[v] = St[(long long)(so * nv + v) * ch.next + tid];
+          un[v] = St[(long long)(sn * nv + v) * ch.next + nt];
+        }
+        const double jq = fabs(d_entropy<D>(c_k, un) - d_entropy<D>(c_k, uo));
+        if (!(jq == jq)) nan = true;
+        jmax = fmax(jmax, jq);
+      }
+    }
+  }
+  fl[tid] = (nan || jmax / Q >= c_k.dm) ? 1 : 0;
+}
+
+// Flags of the extended box's ghost cells: the flag of the cell they
+// replicate (periodic image / outflow clamp).  Slab-axis neighbours owned by
+// another rank were received into extended planes 0 and C+1 (x, mid interior
+// positions) before this runs.
+template <int D>
+__global__ void __launch_bounds__(256) k_kx_mirror(unsigned char* __restrict__ fl, Geo g,
+                                                   Chunk ch, int p0g, int nsa, int nranks) {
+  const long long tid = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (tid >= ch.next) return;
+  const int a = (int)(tid % ch.ex);
+  const long long r1 = tid / ch.ex;
+  const int b = (int)(r1 % ch.em), c = (int)(r1 / ch.em);
+  const int x = a - 1, j = D == 3 ? b - 1 : 0;
+  const bool xin = x >= 0 && x < g.nx, jin = D == 2 || (j >= 0 && j < g.nm);
+  const bool pin = c >= 1 && c <= ch.C;
+  if (xin && jin && pin) return;
+  const int xt = remap(x, g.nx, c_k.bc), jt = D == 3 ? remap(j, g.nm, c_k.bc) : 0;
+  int ct = c;
+  if (!pin) {
+    const int pg = p0g + ch.c0 - 1 + c;  // global plane of this extended plane
+    const bool outside = pg < 0 || pg >= nsa;
+    if (nranks == 1 || (outside && c_k.bc != KFVM_BC_PERIODIC)) {
+      // replicated plane is local: periodic wrap (one rank) or outflow clamp
+      const int pt = remap(pg, nsa, c_k.bc) - p0g;  // local plane index
+      ct = pt - (ch.c0 - 1);
+    } else if (xin && jin) {
+      return;  // received from the neighbouring rank
+    }
+  }
+  fl[tid] = fl[((long long)ct * ch.em + (D == 3 ? jt + 1 : 0)) * ch.ex + (xt + 1)];
+}
+
+#endif

@@ -43,11 +43,13 @@ struct RowCfg {
 
 // FUSE = false: the same row-marching reconstruction writing every face
 // state to St (k_flux follows), for comparison.
-template <int R, bool FUSE>
+// KX (with FUSE = false): KXRCF mode — rows without a flagged cell are
+// skipped, flagged cells get unlimited WENO states (k_limit_states follows).
+template <int R, bool FUSE, bool KX = false>
 __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
     k_stage_row(const double* __restrict__ U, const double* __restrict__ Pr,
                 double* __restrict__ St, double* __restrict__ F, Geo g, Chunk ch, int KZ,
-                int* __restrict__ err) {
+                int* __restrict__ err, const unsigned char* __restrict__ kfl = nullptr) {
   constexpr int D = 2, nv = 4;
   using G = Gen<2, R>;
   using C = RowCfg<R>;
@@ -108,6 +110,14 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
       load_prims(p + 2);
     }
     __pipeline_commit();
+    if constexpr (KX) {
+      const bool mine = active && kfl[(long long)c * ch.ex + a];
+      if (!__syncthreads_or(mine)) {
+        __pipeline_wait_prior(0);
+        __syncthreads();
+        continue;
+      }
+    }
     const int slot0 = (p - R + 4 * C::RING) % C::RING;  // ring slot of row p - R
     auto row = [&](int ozr) -> const double* {        // ozr = oz + R
       const int sl = slot0 + ozr;
@@ -162,7 +172,7 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
       for (int s2 = 0; s2 < NP; ++s2) sW[lane * (NP * nv + 1) + s2 * nv + wv] = w[s2];
     }
     // ---- neighbourhood statistics (same as tile_stats): warp wv -> stat wv
-    {
+    if (!KX) {
       const int stat = wv;
       double r;
       if (stat < 2) {
@@ -200,10 +210,9 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
       for (int v = 0; v < nv; ++v) Ubar[v] = rc[v * C::RX + xr];
       const long long tid = (long long)c * ch.ex + a;
       const bool first = c == cstart, last = c == cend - 1;
-      epilogue_core<D, NP>(err, sW, sS, sTh, T, Ubar, pr0[icn], lane, wv, active,
-                           [&](int s2, int v, double u) {
+      auto store = [&](int s2, int v, double u) {
                              if (!FUSE) {
-                               St[(long long)(s2 * nv + v) * ch.next + tid] = u;
+                               if (!KX || kfl[tid]) St[(long long)(s2 * nv + v) * ch.next + tid] = u;
                                return;
                              }
                              sSt[(s2 * nv + v) * 32 + lane] = u;
@@ -212,7 +221,9 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
                                                (first && s2 >= 2 * RP && s2 < 3 * RP) ||
                                                (last && s2 >= 3 * RP);
                              if (edge) St[(long long)(s2 * nv + v) * ch.next + tid] = u;
-                           });
+                           };
+      epilogue_core<D, NP, decltype(store), !KX>(err, sW, sS, sTh, T, Ubar, pr0[icn], lane, wv,
+                                                 active, store);
     }
     if (!FUSE) {
       __pipeline_wait_prior(0);

@@ -26,6 +26,9 @@
 #ifndef KFVM_U_MINB
 #define KFVM_U_MINB 2
 #endif
+#ifndef KFVM_U_BSMEM_MAX
+#define KFVM_U_BSMEM_MAX (48 * 1024)
+#endif
 
 template <int D, int R>
 struct UCfg {
@@ -44,7 +47,7 @@ struct UCfg {
   static constexpr int PPL = NF * PROW;
   static constexpr int PRING = 4;
   static constexpr int SCW = G::NS * nv * 8;            // beta / c_q per warp
-  static constexpr bool BSMEM = G::NCHUNK * (ND + NPT) * 32 * 8 <= 48 * 1024;
+  static constexpr bool BSMEM = G::NCHUNK * (ND + NPT) * 32 * 8 <= KFVM_U_BSMEM_MAX;
   static constexpr int SB = BSMEM ? G::NCHUNK * (ND + NPT) * 32 : 0;  // B fragments
   static constexpr int PG = NPT <= 3 ? NPT : 4;         // point tiles per pass-2 group
   static constexpr int NG = (NPT + PG - 1) / PG;         // groups (>1: limiter separate)
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
     k_states_u(const double* __restrict__ U, const double* __restrict__ Pr,
                double* __restrict__ St, Geo g, Chunk ch, int KZ, int* __restrict__ err,
                const double* __restrict__ Bd, const double* __restrict__ Bf,
-               const int* __restrict__ gat4) {
+               const int* __restrict__ gat4, const unsigned char* __restrict__ kfl = nullptr) {
   using G = Gen<D, R>;
   using C = UCfg<D, R>;
   constexpr int nv = C::nv, NP = G::NP, NS = G::NS, ND = C::ND, NPT = C::NPT;
@@ -155,6 +158,14 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
       load_prims(p + 2);
     }
     __pipeline_commit();
+    if (kfl) {  // KXRCF: planes of this segment without a flagged cell are skipped
+      const bool mine = active && kfl[((long long)c * ch.em + b) * ch.ex + a];
+      if (!__syncthreads_or(mine)) {
+        __pipeline_wait_prior(0);
+        __syncthreads();
+        continue;
+      }
+    }
     // ring slot of plane p + oz (oz in [-R, R]) without a local pointer array
     const int slot0 = (p - R + 4 * C::RING) % C::RING;  // slot of plane p - R
     auto plane = [&](int ozr) -> const double* {       // ozr = oz + R
@@ -330,10 +341,10 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
           for (int v = 0; v < nv; ++v) cq[v] = sCw[(q * nv + v) * 8 + r8];
         }
       }
-      if constexpr (NG > 1) {
+      if (NG > 1 || kfl) {
         // unlimited states of this group (Phi^-1); k_limit_states limits them
-        if (active) {
-          const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
+        const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
+        if (active && (!kfl || kfl[tid])) {
 #pragma unroll
           for (int n = 0; n < PG; ++n)
 #pragma unroll
@@ -353,6 +364,7 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
     }
     PHASE_MARK(3);
     if constexpr (NG == 1) {
+    if (!kfl) {
     // ---- Phi^-1: conservative states at this lane's points s = 8n + 2k4 + e
     double st[NPT][2][nv];
 #pragma unroll
@@ -463,6 +475,7 @@ __global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
             }
           }
         }
+    }
     }
     }
     PHASE_MARK(4);

@@ -149,6 +149,16 @@ class Solver:
         self._check(self.L.kfvm_gpu_states(self.h, out.ctypes.data), "reconstruct_states")
         return out
 
+    def kxrcf_flags(self, U: Optional[np.ndarray] = None) -> np.ndarray:
+        """KXRCF troubled-cell flags (1 = WENO) of the rank's cells
+        for the state (grid must have kxrcf=True)."""
+        if U is not None:
+            self.set_state(U)
+        shape = self.local_shape[:-1]
+        out = np.zeros(shape, dtype=np.uint8)
+        self._check(self.L.kfvm_gpu_kxrcf_flags(self.h, out.ctypes.data), "kxrcf_flags")
+        return out
+
     def select_dt(self, U: Optional[np.ndarray] = None) -> float:
         """select_dt, fixed-CFL rule."""
         if U is not None:
