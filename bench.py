@@ -203,6 +203,7 @@ def workload_config(w, args):
             "cells": g.ncells, "radius": g.radius, "dim": g.dim, "bc": g.bc,
             "cfl": g.cfl, "config_steps": w.steps,
             "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single",
+            "kxrcf": bool(g.kxrcf),
             "l2": "working set per step (3 state buffers + face-state scratch) exceeds the 126 MB L2"}
 
 
@@ -218,6 +219,8 @@ def main():
     ap.add_argument("--engine", type=int, default=None,
                     help="reconstruction kernel: 0 generic, 1 DFMA, 2 DMMA, 3 fused 2-D stage, "
                          "4 row-marching DFMA (default: 4 in 2-D, 2 in 3-D)")
+    ap.add_argument("--kxrcf", action="store_true",
+                    help="KXRCF troubled-cell mode (S:565): WENO only in flagged cells")
     ap.add_argument("--opt", action="append", default=[], metavar="NAME=VALUE",
                     help="extra solver option (kfvm_gpu_set_option), e.g. overlap=1")
     ap.add_argument("--kz", type=int, default=None,
@@ -226,6 +229,9 @@ def main():
 
     import paper_2401_16543_b200 as K
     w = K.baseline_config(args.config, n=args.n)
+    if args.kxrcf:
+        from dataclasses import replace as _replace
+        w = _replace(w, grid=_replace(w.grid, kxrcf=True))
     if args.steps is None:
         args.steps = w.steps
     args.warmup = max(3, args.warmup)
@@ -290,6 +296,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     launches = s.launch_count - l0
     clk = clocks.stop()
+    kx_frac = float(s.kxrcf_flags().mean()) if g.kxrcf else None
     if dist:
         t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -369,6 +376,8 @@ def main():
                          "traffic": traffic_of(w.index)[0],
                          "traffic_source": traffic_of(w.index)[1]},
             "kernel_ms_per_step": kt,
+            "kxrcf": ({"enabled": True, "flagged_fraction_final_state": kx_frac}
+                      if g.kxrcf else {"enabled": False}),
             "whole_step_fp64_frac": F * value / 1e12 / fp64,
             "gpu_launches": launches,
             "clocks": clk,

@@ -84,7 +84,6 @@ constexpr int npoints(int dim, int R) { return dim == 2 ? 4 * R : 6 * R * R; }
 #include "kfvm_recon.cuh"
 #include "kfvm_recon_u.cuh"
 #include "kfvm_recon_row.cuh"
-#include "kfvm_kxrcf.cuh"
 
 // ------------------------------------------------------------------ k_flux
 template <int DIM>
@@ -174,6 +173,8 @@ __global__ void __launch_bounds__(128) k_flux_edges(const double* __restrict__ S
     face_flux<2, R, 1>(St, F, ch, a, 0, c, (long long)c * ch.fx + a);
   }
 }
+
+#include "kfvm_kxrcf.cuh"
 
 // max of non-negative doubles through their bit patterns (exact, order-free):
 // one atomic per warp instead of one per cell.  Must be called by all lanes
@@ -746,9 +747,11 @@ int kx_flags(kfvm_handle* h, const double* U, const Chunk& ch) {
   tic(h);
   k_pass1<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->St, h->g, ch,
                                                                      h->d_face);
-  k_kx_flag<DIM, R><<<blocks(ch.next, 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->d_flags,
-                                                                 h->g, ch, h->p0, h->nsa);
-  h->launches += 2;
+  // face jumps into the flux scratch (k_flux overwrites it later in the stage)
+  k_kx_face<DIM, R><<<dim3(blocks(ch.nfb, 128), DIM), 128, 0, h->stream>>>(h->St, h->F, h->g, ch);
+  k_kx_flag<DIM><<<blocks(ch.next, 256), 256, 0, h->stream>>>(U, h->Pr, h->F, h->d_flags, h->g,
+                                                              ch, h->p0, h->nsa);
+  h->launches += 3;
   if (h->nranks > 1) {
     NcclApi& N = nccl();
     const bool periodic = h->cfg.bc == KFVM_BC_PERIODIC;

@@ -157,6 +157,17 @@ def gen_case(dim, R):
                 L.append(f"      w[{s_}] = fma(c_f{tag}[{(o + hh) * npnt + s_}], cg, w[{s_}]);")
             L.append("    }")
     L.append("  }")
+    # KXRCF pass 1: unlimited full-stencil r_0 values (stencil 0 = the first
+    # block of the transposed face table), stencil-order chains per point
+    L.append("  // KXRCF pass 1 (S:565): r_0(s) . u over S_0 for one scalar field")
+    L.append("  static __device__ __forceinline__ void pass1(const double (&u)[%d], double (&w)[%d]) {"
+             % (len(full), npnt))
+    for s_ in range(npnt):
+        L.append(f"    w[{s_}] = 0.0;")
+    for h in range(len(full)):
+        for s_ in range(npnt):
+            L.append(f"    w[{s_}] = fma(c_f{tag}[{h * npnt + s_}], u[{h}], w[{s_}]);")
+    L.append("  }")
     L.append("};")
     return "\n".join(L)
 
