@@ -111,7 +111,18 @@ typedef struct kfvm_config {
                          cell (default), 1 = unlimited full-stencil states with
                          WENO only in flagged cells */
   double kxrcf_m;     /* the indicator's power m on Delta (kxrcf.m), 1.5 */
+  int integrator;     /* KFVM_SSPRK3 (BASELINE, default) or KFVM_SSP43: the
+                         reference's SSP(4,3) with embedded SSP(3,2) and a PI
+                         step-size controller, used by
+                         kfvm_gpu_advance_to */
+  double atol, rtol;  /* error-norm tolerances, 1e-4 */
+  double safety;      /* controller safety factor, 0.9 */
+  double dt_min;      /* abort below (0 = none) */
+  double dt_max;      /* clamp above (0 = none) */
 } kfvm_config;
+
+#define KFVM_SSPRK3 0
+#define KFVM_SSP43 1
 
 /* Fill cfg with the reference defaults for the given geometry. */
 void kfvm_config_defaults(kfvm_config* cfg, int dim, int radius, int nx, int ny,
@@ -194,10 +205,16 @@ int kfvm_gpu_step(kfvm_handle* h, double* dt_out);
 /* nsteps SSP-RK3 steps (CUDA-graph captured); dt_seq[nsteps] may be NULL.
  * Replaces advance_to for a fixed step count. */
 int kfvm_gpu_run(kfvm_handle* h, int nsteps, double* dt_seq);
-/* advance_to with fixed-CFL steps: step until t = t_final (the last
- * step is clipped to land on it) or max_steps. */
+/* advance_to: step until t = t_final (the last step is clipped to
+ * land on it) or max_steps.  cfg->integrator = KFVM_SSPRK3: fixed-CFL SSP-RK3
+ * steps; KFVM_SSP43: SSP(4,3) + embedded SSP(3,2) with the PI controller
+ * (accept when the error norm <= 1; max_steps bounds the attempts; *steps =
+ * accepted steps). */
 int kfvm_gpu_advance_to(kfvm_handle* h, double t_final, int max_steps, int* steps,
                         double* t_reached);
+/* Accepted and rejected steps of the last kfvm_gpu_advance_to with the
+ * SSP(4,3) integrator (advance_to run statistics). */
+int kfvm_gpu_step_stats(kfvm_handle* h, int* accepted, int* rejected);
 /* Asynchronous variant on the handle's stream; kfvm_gpu_sync waits and
  * reports device-side errors. */
 int kfvm_gpu_run_async(kfvm_handle* h, int nsteps);

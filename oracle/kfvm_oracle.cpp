@@ -38,6 +38,7 @@ struct Consts {
   double scale[32];  // Delta^(2|alpha|)
   int kx;            // KXRCF on
   double dm;         // Delta^m (host std::pow, the same double the GPU handle uses)
+  double atol, rtol, safety, dt_min, dt_max;  // SSP(4,3) controller
 };
 
 Consts make_consts(const kfvm_config* c, const kfvm_table* t) {
@@ -62,6 +63,11 @@ Consts make_consts(const kfvm_config* c, const kfvm_table* t) {
   k.onemk = 1.0 - c->kappa;
   k.kx = c->kxrcf;
   k.dm = std::pow(c->dx, c->kxrcf_m);
+  k.atol = c->atol;
+  k.rtol = c->rtol;
+  k.safety = c->safety;
+  k.dt_min = c->dt_min;
+  k.dt_max = c->dt_max > 0.0 ? c->dt_max : INFINITY;
   if (t) {
     for (int a = 0; a < t->n_alpha; ++a) {
       const int ord = t->alpha[3 * a] + t->alpha[3 * a + 1] + t->alpha[3 * a + 2];
@@ -732,6 +738,62 @@ inline double combine(int stage, double u0, double uk, double L, double dt) {
   return fma(2.0 / 3.0, w - u0, u0);
 }
 
+// SSP(4,3) with the embedded SSP(3,2), increment form like the
+// SSP-RK3 combine: h = dt/2;
+//   Y2 = u + h L(u);  Y3 = Y2 + h L(Y2);  w = Y3 + h L(Y3);
+//   Y4 = u + (1/3)(w - u);  uhat = u + (2/3)(w - u)  [= u + dt/3 (L1+L2+L3)];
+//   u+ = Y4 + h L(Y4).
+// Stage codes 11..14; stage 13 also returns uhat.
+inline double combine43(int stage, double u0, double uk, double L, double hdt, double* uhat) {
+  const double w = fma(hdt, L, uk);
+  if (stage == 13) {
+    *uhat = fma(2.0 / 3.0, w - u0, u0);
+    return fma(1.0 / 3.0, w - u0, u0);
+  }
+  return w;
+}
+
+// Error norm of the embedded pair: sqrt(sum / N) of
+// ((u+ - uhat) / (atol + rtol |u+|))^2, summed in a pinned three-level order
+// that any slab decomposition reproduces: per row (x, then variables)
+// sequential fma, per plane sequential over its rows, then sequential over
+// the planes of the slab axis.
+double error_norm(const Consts& k, const double* Up, const double* Uh) {
+  const int nv = k.nv;
+  const int nrow = k.dim == 3 ? k.n[1] : 1, npl = k.n[k.dim - 1];
+  const int nx = k.n[0];
+  double s = 0.0;
+  for (int p = 0; p < npl; ++p) {
+    double pl = 0.0;
+    for (int j = 0; j < nrow; ++j) {
+      const size_t o = ((size_t)p * nrow + j) * nx * nv;
+      double r = 0.0;
+      for (int i = 0; i < nx * nv; ++i) {
+        const double q = (Up[o + i] - Uh[o + i]) / fma(k.rtol, std::fabs(Up[o + i]), k.atol);
+        r = fma(q, q, r);
+      }
+      pl = pl + r;
+    }
+    s = s + pl;
+  }
+  return std::sqrt(s / ((double)ncells(k) * nv));
+}
+
+// PI step-size controller (orders 3/2): on acceptance
+// fac = clamp(safety * e^(-0.7/3) * e_prev^(0.4/3), 0.2, 5) with
+// e = max(err, 1e-10) (a zero estimate saturates at 5x); on rejection
+// fac = max(0.2, safety * err^(-1/3)) (0.2 for a NaN estimate).  Powers by the
+// pinned kf_pow.
+inline double pi_factor(const Consts& k, bool accept, double err, double err_prev) {
+  if (accept) {
+    const double e = std::fmax(err, 1e-10);
+    const double f = k.safety * kf_pow(e, -0.7 / 3.0) * kf_pow(err_prev, 0.4 / 3.0);
+    return std::fmin(5.0, std::fmax(0.2, f));
+  }
+  if (!(err == err)) return 0.2;
+  return std::fmax(0.2, k.safety * kf_pow(err, -1.0 / 3.0));
+}
+
 int full_rhs(const kfvm_table* t, const Consts& k, const double* U, double* out, int nslabs,
              int nthreads) {
   const int sa = k.dim - 1;
@@ -784,6 +846,14 @@ int kfo_kxrcf_flags(const kfvm_config* cfg, const kfvm_table* t, const double* U
 
 double kfo_pow(double x, double y) { return kf_pow(x, y); }
 
+void kfo_combine43(int stage, long long n, const double* U0, const double* Uk, const double* L,
+                   double dt, double* out, double* uhat) {
+  const double hdt = 0.5 * dt;
+  double dummy;
+  for (long long i = 0; i < n; ++i)
+    out[i] = combine43(stage, U0[i], Uk[i], L[i], hdt, uhat ? uhat + i : &dummy);
+}
+
 int kfo_select_dt(const kfvm_config* cfg, const double* U, double* dt) {
   const Consts k = make_consts(cfg, nullptr);
   double smax = 0.0;
@@ -825,6 +895,64 @@ int kfo_run(const kfvm_config* cfg, const kfvm_table* t, double* U, int nsteps, 
         if (!admissible(k, U + c * k.nv)) return 2;
     }
   }
+  return 0;
+}
+
+// advance_to with SSP(4,3)+SSP(3,2) and the PI controller:
+// attempts until t_final (the last step lands exactly on it) or max_attempts.
+// dt = min(dt_cfl, dt_err) (dt_err = inf before the first estimate), clamped
+// above by dt_max; below dt_min aborts (code 2).  An attempt is accepted when
+// every stage stayed admissible and err <= 1; a rejected attempt leaves u
+// unchanged.  dt_seq receives the accepted steps' dt (up to cap).
+int kfo_advance43(const kfvm_config* cfg, const kfvm_table* t, double* U, double t_final,
+                  int max_attempts, double* dt_seq, int cap, int* stats, double* t_reached,
+                  int nthreads) {
+  const Consts k = make_consts(cfg, t);
+  const size_t n = ncells(k) * k.nv;
+  std::vector<double> Y(n), Z(n), Uh(n), L(n);
+  double tt = 0.0, dt_err = INFINITY, err_prev = 1.0;
+  int nacc = 0, nrej = 0;
+  for (int at = 0; at < max_attempts && tt < t_final; ++at) {
+    double dt;
+    if (kfo_select_dt(cfg, U, &dt)) return 2;
+    dt = std::fmin(dt, dt_err);
+    if (dt < k.dt_min) return 2;  // unstable setup
+    dt = std::fmin(dt, k.dt_max);
+    const double rem = t_final - tt;
+    if (rem < dt) dt = rem;
+    const double hdt = 0.5 * dt;
+    bool ok = true;
+    const double* src = U;
+    double* dst[4] = {Y.data(), Z.data(), Y.data(), Z.data()};
+    for (int st = 0; st < 4 && ok; ++st) {
+      if (full_rhs(t, k, src, L.data(), 1, nthreads)) {
+        ok = false;
+        break;
+      }
+      for (size_t i = 0; i < n; ++i)
+        dst[st][i] = combine43(11 + st, U[i], src[i], L[i], hdt, &Uh[i]);
+      for (size_t c = 0; c < ncells(k) && ok; ++c)
+        if (!admissible(k, dst[st] + c * k.nv)) ok = false;
+      src = dst[st];
+    }
+    const double err = ok ? error_norm(k, Z.data(), Uh.data()) : NAN;
+    const bool accept = ok && err <= 1.0;
+    dt_err = dt * pi_factor(k, accept, err, err_prev);
+    if (accept) {
+      err_prev = std::fmax(err, 1e-10);
+      tt = tt + dt;
+      std::memcpy(U, Z.data(), n * sizeof(double));
+      if (dt_seq && nacc < cap) dt_seq[nacc] = dt;
+      ++nacc;
+    } else {
+      ++nrej;
+    }
+  }
+  if (stats) {
+    stats[0] = nacc;
+    stats[1] = nrej;
+  }
+  if (t_reached) *t_reached = tt;
   return 0;
 }
 

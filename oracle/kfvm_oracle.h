@@ -34,6 +34,11 @@ int kfo_stage(const kfvm_config* cfg, const kfvm_table* t, const double* U0,
  * virtual slab decomposition (halo copies between slabs) of SURVEY §4(iii). */
 int kfo_run(const kfvm_config* cfg, const kfvm_table* t, double* U, int nsteps,
             double* dt_seq, int nslabs, int nthreads);
+/* advance_to with SSP(4,3)+embedded SSP(3,2) and the PI controller
+ * (S:598-616); stats = {accepted, rejected}; dt_seq = accepted dts. */
+int kfo_advance43(const kfvm_config* cfg, const kfvm_table* t, double* U, double t_final,
+                  int max_attempts, double* dt_seq, int cap, int* stats, double* t_reached,
+                  int nthreads);
 /* Same, restricted to the planes [p0, p0+np) of the slab axis of a bigger
  * global grid: one RHS (stage-1 update) of the sub-box, for timing samples. */
 int kfo_sample_stage(const kfvm_config* cfg, const kfvm_table* t, const double* U,
@@ -44,6 +49,9 @@ int kfo_sample_stage(const kfvm_config* cfg, const kfvm_table* t, const double* 
 int kfo_kxrcf_flags(const kfvm_config* cfg, const kfvm_table* t, const double* U,
                     unsigned char* flags, int nthreads);
 double kfo_pow(double x, double y);
+/* SSP(4,3)+SSP(3,2) stage combine, stage codes 11..14 (uhat written at 13). */
+void kfo_combine43(int stage, long long n, const double* U0, const double* Uk, const double* L,
+                   double dt, double* out, double* uhat);
 
 /* Slab pieces for the multi-process decomposition test. */
 int kfo_slab_rhs(const kfvm_config* cfg, const kfvm_table* t, int p0, int np,

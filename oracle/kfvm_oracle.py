@@ -49,7 +49,9 @@ def lib():
             "kfo_weno": (None, [T, C.c_double, C.c_double, P, P, P, P]),
             "kfo_limit": (I, [I, I, P, P, C.c_double, C.c_double, C.c_double, P]),
             "kfo_kxrcf_flags": (I, [CF, T, P, P, I]),
+            "kfo_advance43": (I, [CF, T, P, C.c_double, I, P, I, P, D, I]),
             "kfo_pow": (C.c_double, [C.c_double, C.c_double]),
+            "kfo_combine43": (None, [I, C.c_longlong, P, P, P, C.c_double, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -118,6 +120,18 @@ class Oracle:
         self._chk(self.L.kfo_run(C.byref(self.cfg), self.rset.c_table, _p(U), int(nsteps),
                                  _p(dts), int(nslabs), self.nthreads), "run")
         return U, dts[:nsteps]
+
+    def advance43(self, U, t_final, max_attempts=1000, cap=4096):
+        """SSP(4,3)+SSP(3,2) with the PI controller to t_final: returns
+        (U, accepted dts, n_accepted, n_rejected, t_reached)."""
+        U = np.array(U, dtype=np.float64, copy=True, order="C")
+        dts = np.zeros(cap)
+        st = np.zeros(2, dtype=np.int32)
+        tr = C.c_double()
+        self._chk(self.L.kfo_advance43(C.byref(self.cfg), self.rset.c_table, _p(U),
+                                       float(t_final), int(max_attempts), _p(dts), int(cap),
+                                       _p(st), C.byref(tr), self.nthreads), "advance43")
+        return U, dts[:min(int(st[0]), cap)], int(st[0]), int(st[1]), tr.value
 
     def slab_rhs(self, U_local, p0, np_planes):
         """RHS of planes [p0, p0+np) from the slab's array incl. R+1 halo planes."""

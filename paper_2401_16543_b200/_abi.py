@@ -41,6 +41,8 @@ class KfvmConfig(C.Structure):
         ("dx", C.c_double), ("gamma", C.c_double), ("cfl", C.c_double),
         ("eps", C.c_double), ("kappa", C.c_double), ("flattener_kf", C.c_double),
         ("kxrcf", C.c_int), ("kxrcf_m", C.c_double),
+        ("integrator", C.c_int), ("atol", C.c_double), ("rtol", C.c_double),
+        ("safety", C.c_double), ("dt_min", C.c_double), ("dt_max", C.c_double),
     ]
 
 
@@ -77,6 +79,7 @@ EXPORTS = [
     ("kfvm_gpu_states", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kfvm_gpu_select_dt", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("kfvm_gpu_kxrcf_flags", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kfvm_gpu_step_stats", C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("kfvm_gpu_stage", C.c_int, [C.c_void_p, C.c_int, C.c_double]),
     ("kfvm_gpu_step", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("kfvm_gpu_run", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),

@@ -35,6 +35,12 @@ class GridConfig:
     ell_over_delta: float = 5.0
     kxrcf: bool = False         # kxrcf.enabled: WENO only in flagged cells
     kxrcf_m: float = 1.5        # kxrcf.m
+    integrator: str = "ssprk3"  # "ssprk3" (BASELINE) | "ssp43" (adaptive)
+    atol: float = 1e-4
+    rtol: float = 1e-4
+    safety: float = 0.9
+    dt_min: float = 0.0         # 0 = none
+    dt_max: float = 0.0         # 0 = none
 
     def __post_init__(self):
         if self.dim not in (2, 3):
@@ -43,6 +49,8 @@ class GridConfig:
             raise ValueError("unsupported stencil radius (must be 2 or 3)")
         if self.bc not in ("periodic", "outflow"):
             raise ValueError("bc must be periodic or outflow")
+        if self.integrator not in ("ssprk3", "ssp43"):
+            raise ValueError("integrator must be ssprk3 or ssp43")
         if self.riemann not in ("hllc", "hll"):
             raise ValueError("riemann must be hllc or hll")
         if min(self.nx, self.ny, self.nz) < 1:
@@ -74,6 +82,9 @@ class GridConfig:
         c.gamma, c.cfl, c.eps = self.gamma, self.cfl, self.eps
         c.kappa, c.flattener_kf = self.kappa, self.flattener_kf
         c.kxrcf, c.kxrcf_m = int(bool(self.kxrcf)), float(self.kxrcf_m)
+        c.integrator = 1 if self.integrator == "ssp43" else 0
+        c.atol, c.rtol, c.safety = self.atol, self.rtol, self.safety
+        c.dt_min, c.dt_max = self.dt_min, self.dt_max
         return c
 
 

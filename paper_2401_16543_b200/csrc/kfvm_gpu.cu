@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ F,
                                                 double* __restrict__ Uout, Geo g, Chunk ch,
                                                 int stage, const double* __restrict__ dtp,
                                                 unsigned long long* __restrict__ smax,
-                                                int* __restrict__ err) {
+                                                int* __restrict__ err,
+                                                double* __restrict__ Uhat = nullptr) {
   constexpr int nv = DIM + 2;
   const int nm = DIM == 3 ? g.nm : 1;
   const long long ncell = (long long)g.nx * nm * ch.C;
@@ -230,6 +231,10 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ F,
     const double L = -(acc / c_k.dx);
     if (stage == 0) {
       un[v] = L;
+    } else if (stage > 10) {
+      double uh = 0.0;
+      un[v] = d_combine43(stage, U0[v * g.vstride + ou], Uk[v * g.vstride + ou], L, dt, &uh);
+      if (stage == 13 && valid) Uhat[v * g.vstride + ou] = uh;
     } else {
       un[v] = d_combine(stage, U0[v * g.vstride + ou], Uk[v * g.vstride + ou], L, dt, c_k.c13,
                         c_k.c23);
@@ -384,6 +389,7 @@ struct NcclApi {
   int (*Send)(const void*, size_t, int, int, nccl_comm, cudaStream_t);
   int (*Recv)(void*, size_t, int, int, nccl_comm, cudaStream_t);
   int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
+  int (*AllGather)(const void*, void*, size_t, int, nccl_comm, cudaStream_t);
   int (*GroupStart)();
   int (*GroupEnd)();
 };
@@ -402,9 +408,12 @@ NcclApi& nccl() {
   api.Recv = (int (*)(void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclRecv");
   api.AllReduce = (int (*)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(
       h, "ncclAllReduce");
+  api.AllGather = (int (*)(const void*, void*, size_t, int, nccl_comm, cudaStream_t))dlsym(
+      h, "ncclAllGather");
   api.GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
   api.GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
   api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.AllReduce &&
+           api.AllGather &&
            api.GroupStart && api.GroupEnd && api.CommDestroy;
   return api;
 }
@@ -413,6 +422,12 @@ const int kNcclUint64 = 5;  // ncclUint64
 const int kNcclDouble = 8;  // ncclFloat64
 const int kNcclMax = 2;     // ncclMax
 }  // namespace
+
+// SSP(4,3) controller state (device)
+struct Ctl {
+  double t, t_final, dt_err, err_prev, err;
+  int nacc, nrej, accept, done, abort;
+};
 
 struct kfvm_handle {
   kfvm_config cfg{};
@@ -451,6 +466,16 @@ struct kfvm_handle {
   long long launches = 0;
   long long graph_launches = 0;
   long long st_budget = 16LL << 30;
+  int integrator = KFVM_SSPRK3;
+  double* Uh = nullptr;               // SSP(4,3): embedded SSP(3,2) solution
+  double* d_rows = nullptr;           // error-norm row partials [plane][row]
+  double* d_planes = nullptr;         // plane partials, [rank][npmax] after the gather
+  int npmax = 0;
+  struct Ctl* d_ctl = nullptr;        // controller state on the device
+  int* d_nps = nullptr;               // planes per rank
+  cudaGraphExec_t graph43 = nullptr;
+  int nacc43 = 0, nrej43 = 0;
+  long long graph43_launches = 0;
   bool kx = false;                    // KXRCF two-pass reconstruction
   unsigned char* d_flags = nullptr;   // KXRCF flags of the extended box
   std::string err;
@@ -649,12 +674,13 @@ void update(kfvm_handle* h, const Chunk& ch, const double* U0, const double* Uk,
   const long long n = (long long)h->g.nx * (h->dim == 3 ? h->g.nm : 1) * ch.C;
   tic(h);
   unsigned long long* sm = stage == 3 ? h->d_smax : nullptr;
+  double* uh = stage == 13 ? h->Uh : nullptr;
   if (h->dim == 2)
     k_update<2><<<blocks(n, 256), 256, 0, h->stream>>>(h->F, U0, Uk, Uout, h->g, ch, stage,
-                                                       h->d_dt_cur, sm, h->d_err);
+                                                       h->d_dt_cur, sm, h->d_err, uh);
   else
     k_update<3><<<blocks(n, 256), 256, 0, h->stream>>>(h->F, U0, Uk, Uout, h->g, ch, stage,
-                                                       h->d_dt_cur, sm, h->d_err);
+                                                       h->d_dt_cur, sm, h->d_err, uh);
   h->launches++;
   toc(h, &h->t_update);
 }
@@ -843,6 +869,111 @@ int run_stage(kfvm_handle* h, const double* Uin, double* Uout, int stage) {
   return KFVM_OK;
 }
 
+// ----------------------------------------------- SSP(4,3) + PI controller
+// (oracle kfo_advance43): dt from the CFL limit and the
+// controller, 4 stages, the pinned three-level error-norm sum, accept/reject.
+__global__ void k_dt43(const unsigned long long* __restrict__ smax, Ctl* c, double* dt_cur) {
+  if (c->done || c->abort || !(c->t < c->t_final)) {
+    c->done = 1;
+    *dt_cur = 0.0;
+    return;
+  }
+  double dt = (c_k.cfl * c_k.dx) / __longlong_as_double((long long)*smax);
+  if (!(dt > 0.0) || !isfinite(dt)) {
+    c->abort = 1;
+    *dt_cur = 0.0;
+    return;
+  }
+  dt = fmin(dt, c->dt_err);
+  if (dt < c_k.dt_min) {  // unstable setup
+    c->abort = 1;
+    *dt_cur = 0.0;
+    return;
+  }
+  dt = fmin(dt, c_k.dt_max);
+  const double rem = c->t_final - c->t;
+  if (rem < dt) dt = rem;
+  *dt_cur = dt;
+}
+
+// row partials: sequential over x, then variables, of q^2 (fma)
+template <int D>
+__global__ void k_err_rows(const double* __restrict__ Up, const double* __restrict__ Uh,
+                           double* __restrict__ rows, Geo g) {
+  constexpr int nv = D + 2;
+  const int nrow = D == 3 ? g.nm : 1;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)nrow * g.np_loc) return;
+  const int j = (int)(t % nrow), p = (int)(t / nrow);
+  const long long base = (long long)(p + g.H) * g.pstride + (long long)j * g.nx;
+  double r = 0.0;
+  for (int x = 0; x < g.nx; ++x)
+#pragma unroll
+    for (int v = 0; v < nv; ++v) {
+      const long long i = v * g.vstride + base + x;
+      const double up = Up[i];
+      const double q = (up - Uh[i]) / fma(c_k.rtol, fabs(up), c_k.atol);
+      r = fma(q, q, r);
+    }
+  rows[t] = r;
+}
+
+__global__ void k_err_planes(const double* __restrict__ rows, double* __restrict__ planes,
+                             int nrow, int np) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  double pl = 0.0;
+  for (int j = 0; j < nrow; ++j) pl = pl + rows[(long long)p * nrow + j];
+  planes[p] = pl;
+}
+
+__device__ double d_pi_factor(bool accept, double err, double err_prev) {
+  if (accept) {
+    const double e = fmax(err, 1e-10);
+    const double f = c_k.safety * d_kf_pow(e, -0.7 / 3.0) * d_kf_pow(err_prev, 0.4 / 3.0);
+    return fmin(5.0, fmax(0.2, f));
+  }
+  if (!(err == err)) return 0.2;
+  return fmax(0.2, c_k.safety * d_kf_pow(err, -1.0 / 3.0));
+}
+
+// planes: [rank][npmax] (global plane order = rank order); nps: planes per rank
+__global__ void k_ctl43(Ctl* c, const double* __restrict__ planes, const int* __restrict__ nps,
+                        int nranks, int npmax, double ncomp, int* err, const double* dt_cur,
+                        double* dt_seq, int cap) {
+  if (c->done || c->abort) {
+    c->accept = 0;
+    *err = 0;
+    return;
+  }
+  double sum = 0.0;
+  for (int r = 0; r < nranks; ++r)
+    for (int p = 0; p < nps[r]; ++p) sum = sum + planes[(long long)r * npmax + p];
+  const bool ok = *err == 0;
+  *err = 0;
+  const double e = ok ? sqrt(sum / ncomp) : __longlong_as_double(0x7ff8000000000000LL);
+  const bool accept = ok && e <= 1.0;
+  const double dt = *dt_cur;
+  c->dt_err = dt * d_pi_factor(accept, e, c->err_prev);
+  c->err = e;
+  if (accept) {
+    c->err_prev = fmax(e, 1e-10);
+    c->t = c->t + dt;
+    if (c->nacc < cap) dt_seq[c->nacc] = dt;
+    c->nacc += 1;
+  } else {
+    c->nrej += 1;
+  }
+  c->accept = accept ? 1 : 0;
+}
+
+__global__ void k_accept43(const Ctl* c, double* __restrict__ U0, const double* __restrict__ Up,
+                           long long n) {
+  if (!c->accept) return;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) U0[t] = Up[t];
+}
+
 int enqueue_dt(kfvm_handle* h) {
   int rc = reduce_smax(h);
   if (rc) return rc;
@@ -874,6 +1005,40 @@ int enqueue_speed(kfvm_handle* h) {
   return KFVM_OK;
 }
 
+// one SSP(4,3) attempt (graph-captured by kfvm_gpu_advance_to)
+int enqueue_attempt43(kfvm_handle* h) {
+  int rc = enqueue_speed(h);
+  if (rc) return rc;
+  if ((rc = reduce_smax(h))) return rc;
+  k_dt43<<<1, 1, 0, h->stream>>>(h->d_smax, h->d_ctl, h->d_dt_cur);
+  h->launches++;
+  if ((rc = run_stage(h, h->U0, h->Ua, 11))) return rc;
+  if ((rc = run_stage(h, h->Ua, h->Ub, 12))) return rc;
+  if ((rc = run_stage(h, h->Ub, h->Ua, 13))) return rc;
+  if ((rc = run_stage(h, h->Ua, h->Ub, 14))) return rc;
+  const int nrow = h->dim == 3 ? h->g.nm : 1, np = h->g.np_loc;
+  const long long nr = (long long)nrow * np;
+  if (h->dim == 2)
+    k_err_rows<2><<<blocks(nr, 128), 128, 0, h->stream>>>(h->Ub, h->Uh, h->d_rows, h->g);
+  else
+    k_err_rows<3><<<blocks(nr, 128), 128, 0, h->stream>>>(h->Ub, h->Uh, h->d_rows, h->g);
+  double* loc = h->d_planes + (long long)h->nranks * h->npmax;  // this rank's partials
+  k_err_planes<<<blocks(np, 128), 128, 0, h->stream>>>(h->d_rows, h->nranks > 1 ? loc : h->d_planes,
+                                                       nrow, np);
+  h->launches += 2;
+  if (h->nranks > 1) {
+    if (nccl().AllGather(loc, h->d_planes, (size_t)h->npmax, kNcclDouble, h->comm, h->stream) != 0)
+      return fail(h, KFVM_ERR_DEVICE, "ncclAllGather failed (error norm)");
+  }
+  const double ncomp = (double)h->g.nx * h->g.nm * h->nsa * h->nv;
+  k_ctl43<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_planes, h->d_nps, h->nranks, h->npmax, ncomp,
+                                  h->d_err, h->d_dt_cur, h->d_dt_seq, h->dt_cap);
+  const long long n = h->g.vstride * h->nv;
+  k_accept43<<<blocks(n, 256), 256, 0, h->stream>>>(h->d_ctl, h->U0, h->Ub, n);
+  h->launches += 2;
+  return KFVM_OK;
+}
+
 int check_err(kfvm_handle* h) {
   CK(cudaStreamSynchronize(h->stream));
   int e = 0;
@@ -885,12 +1050,16 @@ int check_err(kfvm_handle* h) {
   return KFVM_OK;
 }
 
+void drop_graphs(kfvm_handle* h) {
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->graph43) cudaGraphExecDestroy(h->graph43);
+  h->graph = nullptr;
+  h->graph43 = nullptr;
+}
+
 int ensure_dt_cap(kfvm_handle* h, int n) {
   if (n <= h->dt_cap) return KFVM_OK;
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);
   if (h->d_dt_seq) cudaFree(h->d_dt_seq);
   h->d_dt_seq = nullptr;
   CK(cudaMalloc(&h->d_dt_seq, sizeof(double) * n));
@@ -1061,6 +1230,12 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   k.onemk = 1.0 - cfg->kappa;
   k.c13 = 1.0 / 3.0;
   k.c23 = 2.0 / 3.0;
+  k.atol = cfg->atol;
+  k.rtol = cfg->rtol;
+  k.safety = cfg->safety;
+  k.dt_min = cfg->dt_min;
+  k.dt_max = cfg->dt_max > 0.0 ? cfg->dt_max : INFINITY;
+  h->integrator = cfg->integrator;
   k.kx = cfg->kxrcf ? 1 : 0;
   k.dm = std::pow(cfg->dx, cfg->kxrcf_m);  // the oracle computes the same std::pow
   h->kx = cfg->kxrcf != 0;
@@ -1154,6 +1329,28 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     bad(cudaMalloc(&h->St, h->st_elems * sizeof(double)), "cudaMalloc states");
     bad(cudaMalloc(&h->F, h->f_elems * sizeof(double)), "cudaMalloc flux");
   }
+  if (h->integrator == KFVM_SSP43 && rc == KFVM_OK) {
+    const int nrow = h->dim == 3 ? h->g.nm : 1;
+    h->npmax = (h->nsa + h->nranks - 1) / h->nranks;
+    bad(cudaMalloc(&h->Uh, (size_t)h->g.vstride * h->nv * sizeof(double)), "cudaMalloc uhat");
+    bad(cudaMalloc(&h->d_rows, (size_t)nrow * h->g.np_loc * sizeof(double)), "cudaMalloc rows");
+    bad(cudaMalloc(&h->d_planes, (size_t)(h->nranks + 1) * h->npmax * sizeof(double)),
+        "cudaMalloc planes");
+    bad(cudaMalloc(&h->d_ctl, sizeof(Ctl)), "cudaMalloc ctl");
+    std::vector<int> nps(h->nranks);
+    for (int r = 0; r < h->nranks; ++r) {
+      int q0, nq;
+      kfvm_slab_range(h->nsa, h->nranks, r, &q0, &nq);
+      nps[r] = nq;
+    }
+    bad(cudaMalloc(&h->d_nps, sizeof(int) * h->nranks), "cudaMalloc nps");
+    if (rc == KFVM_OK) {
+      bad(cudaMemcpy(h->d_nps, nps.data(), sizeof(int) * h->nranks, cudaMemcpyHostToDevice), "nps");
+      bad(cudaMemset(h->Uh, 0, (size_t)h->g.vstride * h->nv * sizeof(double)), "memset");
+      bad(cudaMemset(h->d_planes, 0, (size_t)(h->nranks + 1) * h->npmax * sizeof(double)),
+          "memset");
+    }
+  }
   bad(cudaMalloc(&h->d_dt_cur, sizeof(double)), "cudaMalloc dt");
   bad(cudaMalloc(&h->d_smax, sizeof(unsigned long long)), "cudaMalloc smax");
   bad(cudaMalloc(&h->d_tt, 2 * sizeof(double)), "cudaMalloc t");
@@ -1202,12 +1399,14 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
 extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
   if (!h) return;
   if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->graph43) cudaGraphExecDestroy(h->graph43);
   if (h->comm) nccl().CommDestroy(h->comm);
   for (void* p : {(void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
                   (void*)h->aos, (void*)h->d_face, (void*)h->d_deriv, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
                   (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_tt,
-                  (void*)h->d_flags})
+                  (void*)h->d_flags, (void*)h->Uh, (void*)h->d_rows, (void*)h->d_planes,
+                  (void*)h->d_ctl, (void*)h->d_nps})
     if (p) cudaFree(p);
   if (h->stream) cudaStreamDestroy(h->stream);
   if (h->s_halo) cudaStreamDestroy(h->s_halo);
@@ -1407,8 +1606,59 @@ extern "C" int kfvm_gpu_step(kfvm_handle* h, double* dt_out) {
 
 // advance_to with fixed-CFL steps: runs until t = t_final (the last
 // step is clipped) or max_steps; *t_reached is the simulation time reached.
+// advance_to with SSP(4,3)+SSP(3,2) and the PI controller: graph-
+// replayed attempts until t_final, an abort, or max_attempts.
+int advance43(kfvm_handle* h, double t_final, int max_attempts, int* steps, double* t_reached) {
+  if ((int)ensure_dt_cap(h, 4096)) return KFVM_ERR_DEVICE;
+  Ctl c0{};
+  c0.t = 0.0;
+  c0.t_final = t_final;
+  c0.dt_err = INFINITY;
+  c0.err_prev = 1.0;
+  CK(cudaMemcpyAsync(h->d_ctl, &c0, sizeof(c0), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
+  if (!h->graph43) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    const long long l0 = h->launches;
+    int rc = enqueue_attempt43(h);
+    cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(h, KFVM_ERR_DEVICE, "graph capture failed");
+    CK(cudaGraphInstantiate(&h->graph43, graph, 0));
+    cudaGraphDestroy(graph);
+    h->graph43_launches = h->launches - l0;
+    h->launches = l0;
+  }
+  Ctl c = c0;
+  int attempts = 0;
+  while (attempts < max_attempts) {
+    const int n = std::min(8, max_attempts - attempts);
+    for (int i = 0; i < n; ++i) CK(cudaGraphLaunch(h->graph43, h->stream));
+    h->launches += h->graph43_launches * n;
+    attempts += n;
+    CK(cudaMemcpyAsync(&c, h->d_ctl, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (c.abort) return fail(h, KFVM_ERR_RUNTIME, "dt below dt_min or not finite (S:611)");
+    if (c.done || !(c.t < t_final)) break;
+  }
+  h->nacc43 = c.nacc;
+  h->nrej43 = c.nrej;
+  if (steps) *steps = c.nacc;
+  if (t_reached) *t_reached = c.t;
+  CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_step_stats(kfvm_handle* h, int* accepted, int* rejected) {
+  if (accepted) *accepted = h->nacc43;
+  if (rejected) *rejected = h->nrej43;
+  return KFVM_OK;
+}
+
 extern "C" int kfvm_gpu_advance_to(kfvm_handle* h, double t_final, int max_steps, int* steps,
                                    double* t_reached) {
+  if (h->integrator == KFVM_SSP43) return advance43(h, t_final, max_steps, steps, t_reached);
   double tt[2] = {0.0, t_final};
   CK(cudaMemcpyAsync(h->d_tt, tt, sizeof(tt), cudaMemcpyHostToDevice, h->stream));
   int done = 0;
@@ -1462,27 +1712,18 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
     } else {
       h->engine = value ? 2 : 0;
     }
-    if (h->graph) {
-      cudaGraphExecDestroy(h->graph);
-      h->graph = nullptr;
-    }
+    drop_graphs(h);
     return KFVM_OK;
   }
   if (n == "overlap") {
     h->overlap = value != 0;
-    if (h->graph) {
-      cudaGraphExecDestroy(h->graph);
-      h->graph = nullptr;
-    }
+    drop_graphs(h);
     return KFVM_OK;
   }
   if (n == "kz") {
     if (value < 1) return fail(h, KFVM_ERR_CONFIG, "kz must be >= 1");
     h->kz = (int)value;
-    if (h->graph) {
-      cudaGraphExecDestroy(h->graph);
-      h->graph = nullptr;
-    }
+    drop_graphs(h);
     return KFVM_OK;
   }
   if (n == "timing") {
@@ -1500,10 +1741,7 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
       c = value / per_plane - 2;
     }
     c = std::max(1LL, std::min(c, (long long)h->g.np_loc));
-    if (h->graph) {
-      cudaGraphExecDestroy(h->graph);
-      h->graph = nullptr;
-    }
+    drop_graphs(h);
     cudaFree(h->St);
     cudaFree(h->F);
     h->St = h->F = nullptr;
@@ -1579,10 +1817,7 @@ extern "C" int kfvm_gpu_ic_generate(kfvm_handle* h, const kfvm_ic_params* ic) {
   k_ic_fill<<<blocks(n, 128), 128>>>(dP, h->U0, h->g, h->p0);
   CK(cudaDeviceSynchronize());
   for (void* p : tmp) cudaFree(p);
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);
   CK(cudaMemset(h->d_step, 0, sizeof(int)));
   return KFVM_OK;
 }

@@ -265,6 +265,12 @@ extern "C" void kfvm_config_defaults(kfvm_config* c, int dim, int radius, int nx
   c->flattener_kf = 0.33;
   c->kxrcf = 0;
   c->kxrcf_m = 1.5;
+  c->integrator = KFVM_SSPRK3;
+  c->atol = 1e-4;
+  c->rtol = 1e-4;
+  c->safety = 0.9;
+  c->dt_min = 0.0;
+  c->dt_max = 0.0;
 }
 
 extern "C" void kfvm_slab_range(int n_global, int nranks, int rank, int* p0, int* np) {

@@ -189,6 +189,12 @@ class Solver:
                                                C.byref(n), C.byref(t)), "advance_to")
         return n.value, t.value
 
+    def step_stats(self) -> tuple:
+        """(accepted, rejected) steps of the last SSP(4,3) advance_to."""
+        a, r = C.c_int(), C.c_int()
+        self._check(self.L.kfvm_gpu_step_stats(self.h, C.byref(a), C.byref(r)), "step_stats")
+        return a.value, r.value
+
     def run_async(self, nsteps: int):
         self._check(self.L.kfvm_gpu_run_async(self.h, int(nsteps)), "run_async")
 
