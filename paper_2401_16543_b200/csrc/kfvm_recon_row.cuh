@@ -76,22 +76,37 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
   const int xr = lane + R;   // the lane's cell in a ring row
   const int icn = lane + 1;  // the lane's cell in a prims row
 
+  // per-thread source offsets (the same for every row)
+  constexpr int NLU = (C::PL + 127) / 128, NLP = (C::PPL + 127) / 128;
+  unsigned offU[NLU], offP[NLP];
+#pragma unroll
+  for (int k = 0; k < NLU; ++k) {
+    const int i = threadIdx.x + 128 * k;
+    const int rx = i % C::RX, v = i / C::RX;
+    offU[k] = i < C::PL ? (unsigned)(v * g.vstride + remap(x0 - R + rx, g.nx, c_k.bc)) : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < NLP; ++k) {
+    const int i = threadIdx.x + 128 * k;
+    const int rx = i % C::NX, f = i / C::NX;
+    offP[k] = i < C::PPL ? (unsigned)(f * g.vstride + remap(x0 - 1 + rx, g.nx, c_k.bc)) : 0u;
+  }
   auto load_row = [&](int p) {
     double* dst = sRing + ((p + 4 * C::RING) % C::RING) * C::PL;
-    const long long pbase = (long long)(p + g.H) * g.pstride;
-    for (int i = threadIdx.x; i < C::PL; i += 128) {
-      const int rx = i % C::RX, v = i / C::RX;
-      const int xx = remap(x0 - R + rx, g.nx, c_k.bc);
-      __pipeline_memcpy_async(dst + i, U + v * g.vstride + pbase + xx, sizeof(double));
+    const double* src = U + (long long)(p + g.H) * g.pstride;
+#pragma unroll
+    for (int k = 0; k < NLU; ++k) {
+      const int i = threadIdx.x + 128 * k;
+      if (i < C::PL) __pipeline_memcpy_async(dst + i, src + offU[k], sizeof(double));
     }
   };
   auto load_prims = [&](int p) {
     double* dst = sPr + ((p + 4 * C::PRING) % C::PRING) * C::PPL;
-    const long long pbase = (long long)(p + g.H) * g.pstride;
-    for (int i = threadIdx.x; i < C::PPL; i += 128) {
-      const int rx = i % C::NX, f = i / C::NX;
-      const int xx = remap(x0 - 1 + rx, g.nx, c_k.bc);
-      __pipeline_memcpy_async(dst + i, Pr + f * g.vstride + pbase + xx, sizeof(double));
+    const double* src = Pr + (long long)(p + g.H) * g.pstride;
+#pragma unroll
+    for (int k = 0; k < NLP; ++k) {
+      const int i = threadIdx.x + 128 * k;
+      if (i < C::PPL) __pipeline_memcpy_async(dst + i, src + offP[k], sizeof(double));
     }
   };
   {

@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log; grep -E "^E " gpurun_out/pytest_gpu.log | head -5
-for c in 2 1 3; do for kx in "--kxrcf"; do
-python bench.py --config $c --steps 5 --warmup 3 --no-cpu $kx 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg $c $kx', '%.3e'%d['value'], d['kxrcf'], {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()})"
+for rep in 1 2; do for v in oldu new; do
+KFVM_LIB=build/libkfvm_$v.so python bench.py --config 3 --steps 3 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', '%.4e'%d['value'], {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()})"
 done; done
