@@ -47,7 +47,11 @@ struct UCfg {
   static constexpr int PPL = NF * PROW;
   static constexpr int PRING = 4;
   static constexpr int SCW = G::NS * nv * 8;            // beta / c_q per warp
-  static constexpr bool BSMEM = G::NCHUNK * (ND + NPT) * 32 * 8 <= KFVM_U_BSMEM_MAX;
+  // 3-D R=2: B fragments from L1 so that 3 CTAs fit per SM (measured 6.6 %
+  // faster than 2 CTAs with B in shared memory, profiles/r01/README.md)
+  static constexpr bool BSMEM =
+      !(D == 3 && R == 2) && G::NCHUNK * (ND + NPT) * 32 * 8 <= KFVM_U_BSMEM_MAX;
+  static constexpr int MINB = D == 3 ? (R == 2 ? 3 : KFVM_U_MINB) : 4;
   static constexpr int SB = BSMEM ? G::NCHUNK * (ND + NPT) * 32 : 0;  // B fragments
   static constexpr int PG = NPT <= 3 ? NPT : 4;         // point tiles per pass-2 group
   static constexpr int NG = (NPT + PG - 1) / PG;         // groups (>1: limiter separate)
@@ -70,7 +74,7 @@ __device__ __forceinline__ double phi_row(const DTransform& T, const double* X, 
 }
 
 template <int D, int R>
-__global__ void __launch_bounds__(128, D == 3 ? KFVM_U_MINB : 4)
+__global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     k_states_u(const double* __restrict__ U, const double* __restrict__ Pr,
                double* __restrict__ St, Geo g, Chunk ch, int KZ, int* __restrict__ err,
                const double* __restrict__ Bd, const double* __restrict__ Bf,
