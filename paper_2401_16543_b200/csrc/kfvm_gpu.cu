@@ -558,7 +558,7 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
         const int KZ = h->kz;
         const long long nb =
             (long long)((ch.ex + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
-        k_states_u<DIM, R><<<(unsigned)nb, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
+        k_states_u<DIM, R, false, true><<<(unsigned)nb, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
             U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, kfl);
       }
     }
@@ -566,9 +566,11 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
       k_states<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g,
                                                                           ch, h->d_err, kfl);
     h->launches++;
-    k_limit_states<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->Pr, h->St,
-                                                                            h->g, ch, h->d_err);
-    h->launches++;
+    if (eng != 4) {  // the 2-D row engine limits every cell itself
+      k_limit_states<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->Pr, h->St,
+                                                                              h->g, ch, h->d_err);
+      h->launches++;
+    }
     toc(h, &h->t_states);
     return;
   }
@@ -771,8 +773,22 @@ void run_planes(kfvm_handle* h, const double* Uin, double* Uout, int stage, int 
 template <int DIM, int R>
 int kx_flags(kfvm_handle* h, const double* U, const Chunk& ch) {
   tic(h);
-  k_pass1<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->St, h->g, ch,
-                                                                     h->d_face);
+  if (DIM == 3 && h->engine == 2) {  // pass 1 on the tensor cores
+    const int KZ = h->kz;
+    const long long nb = (long long)((ch.ex + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
+    k_states_u<DIM, R, true><<<(unsigned)nb, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
+        U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, nullptr);
+  } else if (DIM == 2 && h->engine != 0) {  // pass 1 from the row rings
+    if constexpr (DIM == 2) {
+      const int KZ = h->kz;
+      const long long nb = (long long)((ch.ex + 31) / 32) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
+      k_stage_row<R, false, false, true><<<(unsigned)nb, 128, 0, h->stream>>>(
+          U, h->Pr, h->St, h->F, h->g, ch, KZ, h->d_err, nullptr);
+    }
+  } else {
+    k_pass1<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->St, h->g, ch,
+                                                                       h->d_face);
+  }
   // face jumps into the flux scratch (k_flux overwrites it later in the stage)
   k_kx_face<DIM, R><<<dim3(blocks(ch.nfb, 128), DIM), 128, 0, h->stream>>>(h->St, h->F, h->g, ch);
   k_kx_flag<DIM><<<blocks(ch.next, 256), 256, 0, h->stream>>>(U, h->Pr, h->F, h->d_flags, h->g,
@@ -1146,6 +1162,10 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   CK(cudaMemcpy(h->d_gat4, g4.data(), g4.size() * sizeof(int), cudaMemcpyHostToDevice));
   CK(cudaFuncSetAttribute(k_states_u<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)M::bytes()));
+  CK(cudaFuncSetAttribute(k_states_u<D, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)M::bytes()));
+  CK(cudaFuncSetAttribute(k_states_u<D, R, false, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M::bytes()));
   return KFVM_OK;
 }
 

@@ -43,9 +43,11 @@ struct RowCfg {
 
 // FUSE = false: the same row-marching reconstruction writing every face
 // state to St (k_flux follows), for comparison.
-// KX (with FUSE = false): KXRCF mode — rows without a flagged cell are
-// skipped, flagged cells get unlimited WENO states (k_limit_states follows).
-template <int R, bool FUSE, bool KX = false>
+// KX (with FUSE = false): KXRCF mode — the WENO part runs only for rows
+// holding a flagged cell; every cell is limited here, unflagged ones from
+// their pass-1 states in St.  P1: KXRCF pass 1 — raw conservative values
+// through Gen::pass1 (r_0 vectors), unlimited states to St.
+template <int R, bool FUSE, bool KX = false, bool P1 = false>
 __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
     k_stage_row(const double* __restrict__ U, const double* __restrict__ Pr,
                 double* __restrict__ St, double* __restrict__ F, Geo g, Chunk ch, int KZ,
@@ -125,14 +127,8 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
       load_prims(p + 2);
     }
     __pipeline_commit();
-    if constexpr (KX) {
-      const bool mine = active && kfl[(long long)c * ch.ex + a];
-      if (!__syncthreads_or(mine)) {
-        __pipeline_wait_prior(0);
-        __syncthreads();
-        continue;
-      }
-    }
+    bool anyflag = true;
+    if constexpr (KX) anyflag = __syncthreads_or(active && kfl[(long long)c * ch.ex + a]) != 0;
     const int slot0 = (p - R + 4 * C::RING) % C::RING;  // ring slot of row p - R
     auto row = [&](int ozr) -> const double* {        // ozr = oz + R
       const int sl = slot0 + ozr;
@@ -142,9 +138,24 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
     const double* prm = sPr + ((p - 1 + 4 * C::PRING) % C::PRING) * C::PPL;
     const double* prp = sPr + ((p + 1 + 4 * C::PRING) % C::PRING) * C::PPL;
 
+    const double* rc = row(R);
+    if constexpr (P1) {
+      double u[G::N0], w[NP];
+#pragma unroll
+      for (int h = 0; h < G::N0; ++h)
+        u[h] = row(G::off(h, 1) + R)[wv * C::RX + xr + G::off(h, 0)];
+      G::pass1(u, w);
+      if (active) {
+        const long long tid = (long long)c * ch.ex + a;
+#pragma unroll
+        for (int s2 = 0; s2 < NP; ++s2) St[(long long)(s2 * nv + wv) * ch.next + tid] = w[s2];
+      }
+      __pipeline_wait_prior(0);
+      __syncthreads();
+      continue;
+    }
     // ---- transform of the cell average (identical to tile_transform)
     DTransform T;
-    const double* rc = row(R);
     T.rt = rc[xr];
     T.inv_r = pr0[2 * C::NX + icn];
     T.ut[0] = pr0[3 * C::NX + icn];
@@ -158,7 +169,7 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
       T.ke = 0.5 * ke;
     }
     // ---- stencil values W_wv = (Phi U)_wv (same operations as gather_var)
-    {
+    if (anyflag) {
       double gv[G::N0];
       if (wv == 0) {
 #pragma unroll
@@ -187,7 +198,7 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
       for (int s2 = 0; s2 < NP; ++s2) sW[lane * (NP * nv + 1) + s2 * nv + wv] = w[s2];
     }
     // ---- neighbourhood statistics (same as tile_stats): warp wv -> stat wv
-    if (!KX) {
+    {
       const int stat = wv;
       double r;
       if (stat < 2) {
@@ -227,7 +238,7 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
       const bool first = c == cstart, last = c == cend - 1;
       auto store = [&](int s2, int v, double u) {
                              if (!FUSE) {
-                               if (!KX || kfl[tid]) St[(long long)(s2 * nv + v) * ch.next + tid] = u;
+                               St[(long long)(s2 * nv + v) * ch.next + tid] = u;
                                return;
                              }
                              sSt[(s2 * nv + v) * 32 + lane] = u;
@@ -237,8 +248,9 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
                                                (last && s2 >= 3 * RP);
                              if (edge) St[(long long)(s2 * nv + v) * ch.next + tid] = u;
                            };
-      epilogue_core<D, NP, decltype(store), !KX>(err, sW, sS, sTh, T, Ubar, pr0[icn], lane, wv,
-                                                 active, store);
+      const double* p1 = KX && !(active && kfl[tid]) ? St + tid : nullptr;
+      epilogue_core<D, NP, decltype(store)>(err, sW, sS, sTh, T, Ubar, pr0[icn], lane, wv, active,
+                                            store, p1, ch.next);
     }
     if (!FUSE) {
       __pipeline_wait_prior(0);

@@ -73,7 +73,10 @@ __device__ __forceinline__ double phi_row(const DTransform& T, const double* X, 
   return c_k.gm1 * t;
 }
 
-template <int D, int R>
+// P1: KXRCF pass 1 on the tensor cores — only the chunks of stencil
+// 0, raw conservative U as the A operand, the r_0 face vectors as B, the
+// unlimited states stored as they come out of the accumulators.
+template <int D, int R, bool P1 = false, bool KXM = false>
 __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     k_states_u(const double* __restrict__ U, const double* __restrict__ Pr,
                double* __restrict__ St, Geo g, Chunk ch, int KZ, int* __restrict__ err,
@@ -162,9 +165,13 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
       load_prims(p + 2);
     }
     __pipeline_commit();
-    if (kfl) {  // KXRCF: planes of this segment without a flagged cell are skipped
-      const bool mine = active && kfl[((long long)c * ch.em + b) * ch.ex + a];
-      if (!__syncthreads_or(mine)) {
+    // KXRCF: the WENO passes run only for planes of this segment holding a
+    // flagged cell; the limiter epilogue runs for every cell (unflagged cells
+    // limit their pass-1 states from St)
+    bool anyflag = true;
+    if constexpr (KXM) {  // KXRCF: planes without a flagged cell are skipped
+      anyflag = __syncthreads_or(active && kfl[((long long)c * ch.em + b) * ch.ex + a]) != 0;
+      if (!anyflag) {
         __pipeline_wait_prior(0);
         __syncthreads();
         continue;
@@ -197,9 +204,12 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
       if (D == 3) ke = fma(T.ut[2], T.ut[2], ke);
       T.ke = 0.5 * ke;
     }
+    constexpr int PG = C::PG, NG = C::NG;
+    double V[nv][PG][2];
+    if (anyflag) {
     PHASE_MARK(0);
     // ---- pass 1: derivative columns -> beta_{q,v}
-    {
+    if constexpr (!P1) {
       double acc[nv][ND][2];
 #pragma unroll
       for (int u = 0; u < nv; ++u)
@@ -268,6 +278,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     __syncwarp();
     PHASE_MARK(1);
     // ---- nonlinear weights: lane k4 handles variables v = k4 (+4)
+    if (!P1)
     for (int v = k4; v < nv; v += 4) {
       double wt[NS];
 #pragma unroll
@@ -293,8 +304,6 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     // ends as the WENO-AO value (oracle weno_field order).  Point tiles in
     // groups of PG (registers); with more than one group the limited states
     // are produced by k_limit_states from the unlimited ones stored here.
-    constexpr int PG = C::PG, NG = C::NG;
-    double V[nv][PG][2];
 #pragma unroll
     for (int grp = 0; grp < NG; ++grp) {
       const int t0 = grp * PG;
@@ -305,7 +314,8 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
       int q = 0;
       double cq[nv];
 #pragma unroll
-      for (int v = 0; v < nv; ++v) cq[v] = sCw[v * 8 + r8];
+      for (int v = 0; v < nv; ++v) cq[v] = P1 ? 1.0 : sCw[v * 8 + r8];
+      constexpr int NCK = P1 ? G::kc(0) : G::NCHUNK;  // pass 1: stencil 0 only
       // software pipeline: fragments of chunk ck+1 load while chunk ck issues
       double av[nv], bv[PG];
       {
@@ -317,8 +327,8 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
         for (int n = 0; n < PG; ++n) bv[n] = t0 + n < NPT ? Bfp[(t0 + n) * 32 + lane] : 0.0;
       }
 #pragma unroll 1
-      for (int ck = 0; ck < G::NCHUNK; ++ck) {
-        const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
+      for (int ck = 0; ck < NCK; ++ck) {
+        const int cn = ck + 1 < NCK ? ck + 1 : ck;
         const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
         const double* ap = plane(oz + R) + inpl + cidx;
         double an[nv], bn[PG];
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
           bn[n] = t0 + n < NPT ? Bfp[(cn * NPT + t0 + n) * 32 + lane] : 0.0;
         double aw[nv];  // c_q (Phi U)_v at the slot, with this lane's cell's Phi
 #pragma unroll
-        for (int v = 0; v < nv; ++v) aw[v] = cq[v] * phi_row<D>(T, av, v);
+        for (int v = 0; v < nv; ++v) aw[v] = P1 ? av[v] : cq[v] * phi_row<D>(T, av, v);
 #pragma unroll
         for (int n = 0; n < PG; ++n)
           if (t0 + n < NPT)
@@ -339,16 +349,27 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
         for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
         for (int n = 0; n < PG; ++n) bv[n] = bn[n];
-        if ((sQ[ck] & 256) && q + 1 < NS) {
+        if (!P1 && (sQ[ck] & 256) && q + 1 < NS) {
           ++q;
 #pragma unroll
           for (int v = 0; v < nv; ++v) cq[v] = sCw[(q * nv + v) * 8 + r8];
         }
       }
-      if (NG > 1 || kfl) {
+      if (P1 && active) {  // pass-1 states are conservative already
+        const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
+#pragma unroll
+        for (int n = 0; n < PG; ++n)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int sp = 8 * (t0 + n) + 2 * k4 + e;
+            if (t0 + n < NPT && sp < NP)
+#pragma unroll
+              for (int v = 0; v < nv; ++v) St[(long long)(sp * nv + v) * ch.next + tid] = V[v][n][e];
+          }
+      } else if (NG > 1 || KXM) {
         // unlimited states of this group (Phi^-1); k_limit_states limits them
         const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
-        if (active && (!kfl || kfl[tid])) {
+        if (active && (!KXM || kfl[tid])) {
 #pragma unroll
           for (int n = 0; n < PG; ++n)
 #pragma unroll
@@ -366,9 +387,10 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
         }
       }
     }
+    }
     PHASE_MARK(3);
-    if constexpr (NG == 1) {
-    if (!kfl) {
+    if constexpr (NG == 1 && !P1 && !KXM) {
+    {
     // ---- Phi^-1: conservative states at this lane's points s = 8n + 2k4 + e
     double st[NPT][2][nv];
 #pragma unroll

@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_states_u -s 3 -c 1 -o gpurun_out/prof_u32b python tools/profile_step.py --config 3 --n 128 --steps 2 > gpurun_out/ncu1.log 2>&1; tail -1 gpurun_out/ncu1.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_kx2.csv python bench.py --config 2 --steps 2 --warmup 3 --no-cpu --kxrcf > gpurun_out/ncu_l.log 2>&1; tail -1 gpurun_out/ncu_l.log | cut -c1-80
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_kx3.csv python bench.py --config 3 --steps 1 --warmup 3 --no-cpu --kxrcf > gpurun_out/ncu_l3.log 2>&1; tail -1 gpurun_out/ncu_l3.log | cut -c1-80
