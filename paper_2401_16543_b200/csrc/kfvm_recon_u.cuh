@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
   {
     const int p = ch.c0 - 1 + cstart;
     for (int oz = -R; oz <= R; ++oz) load_plane(p + oz);
-    for (int oz = -1; oz <= 1; ++oz) load_prims(p + oz);
+    if (!P1)  // pass 1 needs neither the transform nor the limiter statistics
+      for (int oz = -1; oz <= 1; ++oz) load_prims(p + oz);
     __pipeline_commit();
     __pipeline_wait_prior(0);
   }
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     const int p = ch.c0 - 1 + c;
     if (c + 1 < cend) {
       load_plane(p + R + 1);
-      load_prims(p + 2);
+      if (!P1) load_prims(p + 2);
     }
     __pipeline_commit();
     // KXRCF: the WENO passes run only for planes of this segment holding a
