@@ -121,6 +121,14 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
   const int a = seg * 32 + cidx;  // extended x index of this lane's cell
   const bool active = a < ch.ex;
   const int xr = cidx + R;            // the cell's x in the region
+  if constexpr (KXM) {  // KXRCF: a tile without a flagged cell has nothing to do
+    bool any = false;
+    for (int i = threadIdx.x; i < 32 * (cend - cstart); i += 128) {
+      const int ai = seg * 32 + (i & 31), ci = cstart + (i >> 5);
+      any |= ai < ch.ex && kfl[((long long)ci * ch.em + b) * ch.ex + ai];
+    }
+    if (!__syncthreads_or(any)) return;
+  }
 
   // x indices (remapped) of the region columns this thread copies
   auto load_plane = [&](int p) {  // region plane p -> ring slot
