@@ -158,12 +158,24 @@ void weno_field(const kfvm_table* t, const Consts& k, const double* g, double* b
     const int N = t->size[q];
     const int* gat = t->gather + t->cell_offset[q];
     const double* D = t->deriv + (size_t)t->cell_offset[q] * t->n_alpha;
-    double beta = 0.0;
+    // beta_q = sum_alpha Delta^(2|alpha|) d_alpha^2 summed in four
+    // interleaved partial chains — alpha = 8n + 2j + e goes to partial j, in
+    // (n, e) order — combined as (p0 + p1) + (p2 + p3).  This is the order in
+    // which the tensor-core engine's quads hold the derivative columns
+    // (DESIGN.md §4), so no cross-lane sequential chain is needed.
+    double d[32];
     for (int a = 0; a < t->n_alpha; ++a) {
-      double d = 0.0;
-      for (int h = 0; h < N; ++h) d = fma(D[a * N + h], g[gat[h]], d);
-      beta = fma(k.scale[a], d * d, beta);
+      d[a] = 0.0;
+      for (int h = 0; h < N; ++h) d[a] = fma(D[a * N + h], g[gat[h]], d[a]);
     }
+    double part[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = 0; j < 4; ++j)
+      for (int n = 0; 8 * n < t->n_alpha; ++n)
+        for (int e = 0; e < 2; ++e) {
+          const int a = 8 * n + 2 * j + e;
+          if (a < t->n_alpha) part[j] = fma(k.scale[a], d[a] * d[a], part[j]);
+        }
+    const double beta = (part[0] + part[1]) + (part[2] + part[3]);
     if (beta_out) beta_out[q] = beta;
     // P eq. nlinWts: gamma_q / (beta_q^2 + eps), evaluated as gamma_q * (1 / d)
     wt[q] = t->gamma_lin[q] * (1.0 / fma(beta, beta, k.eps));

@@ -257,20 +257,27 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
 #pragma unroll
         for (int n = 0; n < ND; ++n) bv[n] = bn[n];
         if (sQ[ck] & 256) {
-          // acc[v][n][e]: variable v of cell r8, alpha = 8n + 2k4 + e;
-          // beta_v = sequential chain over alpha (quad shuffles)
-          double (&dv)[nv][ND][2] = acc;
+          // acc[v][n][e]: variable v of cell r8, alpha = 8n + 2k4 + e; each
+          // lane chains its own alphas (partial k4, (n, e) order) and the quad
+          // combines (p0 + p1) + (p2 + p3) (oracle weno_field order; the xor
+          // tree gives every lane that value since + is commutative)
           double bq[nv];
 #pragma unroll
           for (int v = 0; v < nv; ++v) bq[v] = 0.0;
 #pragma unroll
-          for (int al = 0; al < G::NA; ++al) {
-            const int src = (lane & ~3) | ((al & 7) >> 1);
+          for (int n = 0; n < ND; ++n)
 #pragma unroll
-            for (int v = 0; v < nv; ++v) {
-              const double d = __shfl_sync(0xffffffffu, dv[v][al >> 3][al & 1], src);
-              bq[v] = fma(c_t.scale[al], d * d, bq[v]);
+            for (int e = 0; e < 2; ++e) {
+              const int al = 8 * n + 2 * k4 + e;
+              const double sc = al < G::NA ? c_t.scale[al] : 0.0;
+#pragma unroll
+              for (int v = 0; v < nv; ++v)
+                if (al < G::NA) bq[v] = fma(sc, acc[v][n][e] * acc[v][n][e], bq[v]);
             }
+#pragma unroll
+          for (int v = 0; v < nv; ++v) {
+            bq[v] = bq[v] + __shfl_xor_sync(0xffffffffu, bq[v], 1);
+            bq[v] = bq[v] + __shfl_xor_sync(0xffffffffu, bq[v], 2);
           }
           if (k4 == 0) {
 #pragma unroll

@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for kz in 8 16 32 64; do
-python bench.py --config 3 --steps 3 --warmup 3 --no-cpu --kz $kz 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('kz $kz', '%.4e'%d['value'], {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()})"
-done
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log; grep -E "^E |FAILED" gpurun_out/pytest_gpu.log | head -5
+for c in 2 3; do python bench.py --config $c --steps 5 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg $c', '%.4e'%d['value'], d['roofline']['frac'], {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()})"; done
+python bench.py --config 5 --n 256 --steps 2 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg5', '%.4e'%d['value'], d['roofline']['frac'], {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()})"

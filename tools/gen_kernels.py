@@ -120,17 +120,21 @@ def gen_case(dim, R):
     L.append("                                              double inv_g0) {")
     for q in range(ns):
         m, N, o = members[q], sizes[q], offs[q]
+        # beta: four interleaved partials, alpha = 8n + 2j + e -> partial j,
+        # combined as (b0 + b1) + (b2 + b3) (oracle weno_field)
         L.append(f"    double wt{q};")
         L.append("    {")
-        L.append("      double b = 0.0;")
+        L.append("      double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;")
         for a in range(na):
             base = o * na + a * N
             L.append("      {")
             L.append("        double d = 0.0;")
             for hh, h in enumerate(m):
                 L.append(f"        d = fma(c_d{tag}[{base + hh}], g[{h}], d);")
-            L.append(f"        b = fma(sc[{a}], d * d, b);")
+            j = (a & 7) >> 1
+            L.append(f"        b{j} = fma(sc[{a}], d * d, b{j});")
             L.append("      }")
+        L.append("      const double b = (b0 + b1) + (b2 + b3);")
         L.append(f"      wt{q} = gam[{q}] * (1.0 / fma(b, b, eps));")
         L.append("    }")
     L.append("    double sum = wt0;")
