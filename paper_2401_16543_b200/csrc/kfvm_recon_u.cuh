@@ -293,24 +293,34 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     }
     __syncwarp();
     PHASE_MARK(1);
-    // ---- nonlinear weights: lane k4 handles variables v = k4 (+4)
-    if (!P1)
-    for (int v = k4; v < nv; v += 4) {
-      double wt[NS];
+    // ---- nonlinear weights, in two balanced steps: lane k4 forms
+    // omega~ = gamma_q / (beta^2 + eps) for the stencils q = k4 (+4) of every
+    // variable of its cell (the divisions, 10 per lane), then lane k4 sums
+    // and normalises variable v = k4 (+4) — the same operations as one
+    // sequential pass per variable
+    if (!P1) {
 #pragma unroll
-      for (int q = 0; q < NS; ++q) {
-        const double bb = sCw[(q * nv + v) * 8 + r8];
-        wt[q] = c_t.gamma_lin[q] * (1.0 / fma(bb, bb, c_k.eps));
+      for (int q = k4; q < NS; q += 4)
+#pragma unroll
+        for (int v = 0; v < nv; ++v) {
+          const double bb = sCw[(q * nv + v) * 8 + r8];
+          sCw[(q * nv + v) * 8 + r8] = c_t.gamma_lin[q] * (1.0 / fma(bb, bb, c_k.eps));
+        }
+      __syncwarp();
+      for (int v = k4; v < nv; v += 4) {
+        double wt[NS];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) wt[q] = sCw[(q * nv + v) * 8 + r8];
+        double sum = wt[0];
+#pragma unroll
+        for (int q = 1; q < NS; ++q) sum = sum + wt[q];
+        const double inv_sum = 1.0 / sum;
+        const double c0 = (wt[0] * inv_sum) * c_t.inv_g0;
+        sCw[v * 8 + r8] = c0;
+#pragma unroll
+        for (int q = 1; q < NS; ++q)
+          sCw[(q * nv + v) * 8 + r8] = fma(-c0, c_t.gamma_lin[q], wt[q] * inv_sum);
       }
-      double sum = wt[0];
-#pragma unroll
-      for (int q = 1; q < NS; ++q) sum = sum + wt[q];
-      const double inv_sum = 1.0 / sum;
-      const double c0 = (wt[0] * inv_sum) * c_t.inv_g0;
-      sCw[v * 8 + r8] = c0;
-#pragma unroll
-      for (int q = 1; q < NS; ++q)
-        sCw[(q * nv + v) * 8 + r8] = fma(-c0, c_t.gamma_lin[q], wt[q] * inv_sum);
     }
     __syncwarp();
     PHASE_MARK(2);
