@@ -148,6 +148,10 @@ inline void from_recon(int dim, const Transform& T, double inv_gm1, const double
 }
 
 // ------------------------------------------------------------------- WENO-AO
+// First derivative index evaluated as four slot chains (3-D only; 2-D keeps
+// every derivative a single stencil-order chain).
+inline int kfo_alpha_tail(int dim, int n_alpha) { return dim == 3 ? 8 * (n_alpha / 8) : n_alpha; }
+
 // beta_q, omega_q and the WENO-AO values at every face point for one scalar
 // field g on S0.  Dot products accumulate in stencil order.
 void weno_field(const kfvm_table* t, const Consts& k, const double* g, double* beta_out,
@@ -163,10 +167,29 @@ void weno_field(const kfvm_table* t, const Consts& k, const double* g, double* b
     // (n, e) order — combined as (p0 + p1) + (p2 + p3).  This is the order in
     // which the tensor-core engine's quads hold the derivative columns
     // (DESIGN.md §4), so no cross-lane sequential chain is needed.
+    // d_alpha = d_alpha . g as the stencil-order fma chain, except in 3-D for
+    // the tail alphas >= 8 floor(n_alpha / 8) (the columns that would fill
+    // only part of an 8-wide tensor-core tile): those are four slot chains —
+    // entry h goes to slot (h + pad_q) mod 4, pad_q = (-N_q) mod 4, each slot
+    // chain in stencil order — combined as (s0 + s1) + (s2 + s3).  That is the
+    // order in which the lanes of a quad hold the 4-entry DMMA chunks (front
+    // padded), so the tensor-core engine computes them with per-lane DFMA
+    // instead of a mostly-empty DMMA tile.
+    const int a_tail = kfo_alpha_tail(t->dim, t->n_alpha);
+    const int pad = (4 - N % 4) % 4;
     double d[32];
     for (int a = 0; a < t->n_alpha; ++a) {
-      d[a] = 0.0;
-      for (int h = 0; h < N; ++h) d[a] = fma(D[a * N + h], g[gat[h]], d[a]);
+      if (a < a_tail) {
+        d[a] = 0.0;
+        for (int h = 0; h < N; ++h) d[a] = fma(D[a * N + h], g[gat[h]], d[a]);
+      } else {
+        double sl[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int h = 0; h < N; ++h) {
+          const int j = (h + pad) % 4;
+          sl[j] = fma(D[a * N + h], g[gat[h]], sl[j]);
+        }
+        d[a] = (sl[0] + sl[1]) + (sl[2] + sl[3]);
+      }
     }
     double part[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = 0; j < 4; ++j)

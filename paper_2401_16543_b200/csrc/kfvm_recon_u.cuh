@@ -34,7 +34,11 @@ template <int D, int R>
 struct UCfg {
   using G = Gen<D, R>;
   static constexpr int nv = D + 2;
-  static constexpr int ND = (G::NA + 7) / 8;
+  static constexpr int ND = (G::NA + 7) / 8;             // derivative tiles in Bd
+  // 3-D: the tail derivative columns (a partial last tile, oracle weno_field)
+  // run as per-lane DFMA slot chains; NDM full tiles go through DMMA
+  static constexpr int NDM = D == 3 ? G::NA / 8 : ND;
+  static constexpr int NT = D == 3 ? G::NA - 8 * NDM : 0;
   static constexpr int NPT = (G::NP + 7) / 8;
   static constexpr int RX = 32 + 2 * R;                 // region x extent
   static constexpr int RY = D == 3 ? 2 * R + 1 : 1;     // region mid extent
@@ -219,43 +223,60 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     PHASE_MARK(0);
     // ---- pass 1: derivative columns -> beta_{q,v}
     if constexpr (!P1) {
-      double acc[nv][ND][2];
+      constexpr int NDM = C::NDM, NT = C::NT, NTA = NT > 0 ? NT : 1;
+      double acc[nv][NDM][2];
+      double tl[nv][NTA];  // tail derivative slot chains (slot k4 of the quad)
 #pragma unroll
-      for (int u = 0; u < nv; ++u)
+      for (int u = 0; u < nv; ++u) {
 #pragma unroll
-        for (int n = 0; n < ND; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+        for (int n = 0; n < NDM; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+#pragma unroll
+        for (int t = 0; t < NTA; ++t) tl[u][t] = 0.0;
+      }
       int q = 0;
-      // software pipeline: fragments of chunk ck+1 load while chunk ck issues
-      double av[nv], bv[ND];
+      // software pipeline: fragments of chunk ck+1 load while chunk ck issues;
+      // a tail weight of column 8 NDM + t at slot k4 is the B fragment word
+      // of lane 4t + k4 in the last tile
+      double av[nv], bv[NDM], bt[NTA];
       {
         const int inpl = sTab[2 * k4], oz = sTab[2 * k4 + 1];
         const double* ap = plane(oz + R) + inpl + cidx;
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = ap[u * C::RROW];
 #pragma unroll
-        for (int n = 0; n < ND; ++n) bv[n] = Bdp[n * 32 + lane];
+        for (int n = 0; n < NDM; ++n) bv[n] = Bdp[n * 32 + lane];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) bt[t] = Bdp[(ND - 1) * 32 + 4 * t + k4];
       }
 #pragma unroll 1
       for (int ck = 0; ck < G::NCHUNK; ++ck) {
         const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
         const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
         const double* ap = plane(oz + R) + inpl + cidx;
-        double an[nv], bn[ND];
+        double an[nv], bn[NDM], btn[NTA];
 #pragma unroll
         for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
 #pragma unroll
-        for (int n = 0; n < ND; ++n) bn[n] = Bdp[(cn * ND + n) * 32 + lane];
+        for (int n = 0; n < NDM; ++n) bn[n] = Bdp[(cn * ND + n) * 32 + lane];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) btn[t] = Bdp[(cn * ND + ND - 1) * 32 + 4 * t + k4];
         double aw[nv];  // W = Phi U at the slot, with this lane's cell's Phi
 #pragma unroll
         for (int v = 0; v < nv; ++v) aw[v] = phi_row<D>(T, av, v);
 #pragma unroll
-        for (int n = 0; n < ND; ++n)
+        for (int n = 0; n < NDM; ++n)
 #pragma unroll
           for (int v = 0; v < nv; ++v) dmma(acc[v][n][0], acc[v][n][1], aw[v], bv[n]);
 #pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+          for (int v = 0; v < nv; ++v) tl[v][t] = fma(bt[t], aw[v], tl[v][t]);
+#pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
-        for (int n = 0; n < ND; ++n) bv[n] = bn[n];
+        for (int n = 0; n < NDM; ++n) bv[n] = bn[n];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) bt[t] = btn[t];
         if (sQ[ck] & 256) {
           // acc[v][n][e]: variable v of cell r8, alpha = 8n + 2k4 + e; each
           // lane chains its own alphas (partial k4, (n, e) order) and the quad
@@ -265,7 +286,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
 #pragma unroll
           for (int v = 0; v < nv; ++v) bq[v] = 0.0;
 #pragma unroll
-          for (int n = 0; n < ND; ++n)
+          for (int n = 0; n < NDM; ++n)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int al = 8 * n + 2 * k4 + e;
@@ -274,6 +295,19 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
               for (int v = 0; v < nv; ++v)
                 if (al < G::NA) bq[v] = fma(sc, acc[v][n][e] * acc[v][n][e], bq[v]);
             }
+          // tail alphas 8 NDM + t: the quad combines the slot chains as
+          // (s0 + s1) + (s2 + s3); partial (t >> 1) takes them in t order
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const int al = 8 * NDM + t;
+#pragma unroll
+            for (int v = 0; v < nv; ++v) {
+              double d = tl[v][t] + __shfl_xor_sync(0xffffffffu, tl[v][t], 1);
+              d = d + __shfl_xor_sync(0xffffffffu, d, 2);
+              if ((t >> 1) == k4) bq[v] = fma(c_t.scale[al], d * d, bq[v]);
+              tl[v][t] = 0.0;
+            }
+          }
 #pragma unroll
           for (int v = 0; v < nv; ++v) {
             bq[v] = bq[v] + __shfl_xor_sync(0xffffffffu, bq[v], 1);
@@ -286,7 +320,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
 #pragma unroll
           for (int u = 0; u < nv; ++u)
 #pragma unroll
-            for (int n = 0; n < ND; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+            for (int n = 0; n < NDM; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
           ++q;
         }
       }

@@ -125,12 +125,22 @@ def gen_case(dim, R):
         L.append(f"    double wt{q};")
         L.append("    {")
         L.append("      double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;")
+        # 3-D tail alphas (>= 8 floor(na/8)): four slot chains, entry hh in
+        # slot (hh + pad) % 4, combined (s0 + s1) + (s2 + s3) (oracle weno_field)
+        a_tail = 8 * (na // 8) if dim == 3 else na
+        pad = (4 - N % 4) % 4
         for a in range(na):
             base = o * na + a * N
             L.append("      {")
-            L.append("        double d = 0.0;")
-            for hh, h in enumerate(m):
-                L.append(f"        d = fma(c_d{tag}[{base + hh}], g[{h}], d);")
+            if a < a_tail:
+                L.append("        double d = 0.0;")
+                for hh, h in enumerate(m):
+                    L.append(f"        d = fma(c_d{tag}[{base + hh}], g[{h}], d);")
+            else:
+                L.append("        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;")
+                for hh, h in enumerate(m):
+                    L.append(f"        s{(hh + pad) % 4} = fma(c_d{tag}[{base + hh}], g[{h}], s{(hh + pad) % 4});")
+                L.append("        const double d = (s0 + s1) + (s2 + s3);")
             j = (a & 7) >> 1
             L.append(f"        b{j} = fma(sc[{a}], d * d, b{j});")
             L.append("      }")
