@@ -23,6 +23,10 @@
 
 #include <cuda_pipeline.h>
 
+#ifndef KFVM_U_UNR  // chunk-loop unroll factor
+#define KFVM_U_UNR 4
+#endif
+constexpr int kUChunkUnroll = KFVM_U_UNR;
 #ifndef KFVM_U_MINB
 #define KFVM_U_MINB 2
 #endif
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
 #pragma unroll
         for (int t = 0; t < NT; ++t) bt[t] = Bdp[(ND - 1) * 32 + 4 * t + k4];
       }
-#pragma unroll 1
+#pragma unroll kUChunkUnroll
       for (int ck = 0; ck < G::NCHUNK; ++ck) {
         const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
         const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
 #pragma unroll
         for (int n = 0; n < PG; ++n) bv[n] = t0 + n < NPT ? Bfp[(t0 + n) * 32 + lane] : 0.0;
       }
-#pragma unroll 1
+#pragma unroll kUChunkUnroll
       for (int ck = 0; ck < NCK; ++ck) {
         const int cn = ck + 1 < NCK ? ck + 1 : ck;
         const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
