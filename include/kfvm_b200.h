@@ -119,6 +119,18 @@ typedef struct kfvm_config {
   double safety;      /* controller safety factor, 0.9 */
   double dt_min;      /* abort below (0 = none) */
   double dt_max;      /* clamp above (0 = none) */
+  /* Navier-Stokes terms (PAPER.md eqs nsVisc/shearTensor/
+   * thermalFlux): face-centre second-order differences of the
+   * cell-average primitives, midpoint rule per face, subtracted from the
+   * face-averaged inviscid flux. */
+  int viscous;        /* 0 = Euler (default), 1 = add the viscous fluxes */
+  double reynolds;    /* Re */
+  double prandtl;     /* Pr, 0.71 */
+  double mach;        /* Ma: temperature T = gamma Ma^2 p / rho */
+  /* Gravity source (PAPER.md eq rtSource): per cell
+   * S = (1/Fr^2) (0, 0, rho, [0,] rho u_2) from the cell averages, added to
+   * the flux divergence.  0 = no source. */
+  double inv_froude2;
 } kfvm_config;
 
 #define KFVM_SSPRK3 0

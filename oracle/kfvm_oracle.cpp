@@ -39,6 +39,8 @@ struct Consts {
   int kx;            // KXRCF on
   double dm;         // Delta^m (host std::pow, the same double the GPU handle uses)
   double atol, rtol, safety, dt_min, dt_max;  // SSP(4,3) controller
+  int visc;                                    // Navier-Stokes terms
+  double inv_re, inv_prre, gmm, g2;            // 1/Re, 1/(Pr Re), gamma Ma^2, 1/Fr^2
 };
 
 Consts make_consts(const kfvm_config* c, const kfvm_table* t) {
@@ -68,6 +70,11 @@ Consts make_consts(const kfvm_config* c, const kfvm_table* t) {
   k.safety = c->safety;
   k.dt_min = c->dt_min;
   k.dt_max = c->dt_max > 0.0 ? c->dt_max : INFINITY;
+  k.visc = c->viscous;
+  k.inv_re = 1.0 / c->reynolds;
+  k.inv_prre = 1.0 / (c->prandtl * c->reynolds);
+  k.gmm = c->gamma * (c->mach * c->mach);
+  k.g2 = c->inv_froude2;
   if (t) {
     for (int a = 0; a < t->n_alpha; ++a) {
       const int ord = t->alpha[3 * a] + t->alpha[3 * a + 1] + t->alpha[3 * a + 2];
@@ -655,6 +662,55 @@ int cell_states_kx(const kfvm_table* t, const Consts& k, const Slab& S, const ui
   return limit_cell(k, t->n_points, st, nbr, nullptr);
 }
 
+// Viscous face flux F^(v) (P eqs nsVisc/shearTensor/thermalFlux,
+// P:615-633) of the face between cell (i,j,kk) - e_d (L) and (i,j,kk) (R):
+// second-order differences of the cell-average primitives (u_1..u_dim,
+// T = gamma Ma^2 p / rho), normal = (R - L) / Delta, tangential = the
+// four-cell average ((L+ - L-) + (R+ - R-)) / (4 Delta); sigma and q at the
+// face centre; face velocity (L + R) / 2; midpoint rule.  Pinned operation
+// order, identical on the device (k_visc).
+inline void prim_vt(const Consts& k, const double* U, double* out) {  // u_1..u_dim, T
+  const double p = pressure(k.dim, U, k.gm1);
+  const double inv_r = 1.0 / U[0];
+  for (int a = 0; a < k.dim; ++a) out[a] = U[1 + a] / U[0];
+  out[k.dim] = k.gmm * (p * inv_r);
+}
+
+void viscous_flux(const Consts& k, const Slab& S, int d, int i, int j, int kk, double* Fv) {
+  const int dim = k.dim, nv = k.nv;
+  int cR[3] = {i, j, kk}, cL[3] = {i, j, kk};
+  cL[d] -= 1;
+  double L[4], R[4];
+  prim_vt(k, S.at(cL[0], cL[1], cL[2]), L);
+  prim_vt(k, S.at(cR[0], cR[1], cR[2]), R);
+  double g[4][3];  // g[f][a] = d phi_f / d x_a, phi = (u_1..u_dim, T)
+  for (int f = 0; f <= dim; ++f) g[f][d] = (R[f] - L[f]) / k.dx;
+  for (int a = 0; a < dim; ++a) {
+    if (a == d) continue;
+    double Lp[4], Lm[4], Rp[4], Rm[4];
+    int o[3] = {0, 0, 0};
+    o[a] = 1;
+    prim_vt(k, S.at(cL[0] + o[0], cL[1] + o[1], cL[2] + o[2]), Lp);
+    prim_vt(k, S.at(cL[0] - o[0], cL[1] - o[1], cL[2] - o[2]), Lm);
+    prim_vt(k, S.at(cR[0] + o[0], cR[1] + o[1], cR[2] + o[2]), Rp);
+    prim_vt(k, S.at(cR[0] - o[0], cR[1] - o[1], cR[2] - o[2]), Rm);
+    for (int f = 0; f <= dim; ++f) g[f][a] = ((Lp[f] - Lm[f]) + (Rp[f] - Rm[f])) / (4.0 * k.dx);
+  }
+  double div = g[0][0];
+  for (int a = 1; a < dim; ++a) div = div + g[a][a];
+  double sig[3];
+  for (int a = 0; a < dim; ++a) {
+    double t = g[a][d] + g[d][a];
+    if (a == d) t = fma(-2.0 / 3.0, div, t);
+    sig[a] = t * k.inv_re;
+  }
+  double e = g[dim][d] * k.inv_prre;
+  for (int a = 0; a < dim; ++a) e = fma(sig[a], 0.5 * (L[a] + R[a]), e);
+  Fv[0] = 0.0;
+  for (int a = 0; a < dim; ++a) Fv[1 + a] = sig[a];
+  Fv[nv - 1] = e;
+}
+
 // RHS over the slab's interior planes.  out: AoS [np planes]
 int slab_rhs(const kfvm_table* t, const Consts& k, const Slab& S, double* out, int nthreads,
              double* states_out = nullptr, const uint8_t* flags = nullptr) {
@@ -726,6 +782,11 @@ int slab_rhs(const kfvm_table* t, const Consts& k, const Slab& S, double* out, i
       riemann(k, d, SL + sL * nv, SR + sR * nv, F);
       for (int v = 0; v < nv; ++v) Fbar[v] = fma(fw[sR], F[v], Fbar[v]);
     }
+    if (k.visc) {
+      double Fv[5];
+      viscous_flux(k, S, d, i, j, kk, Fv);
+      for (int v = 0; v < nv; ++v) Fbar[v] = Fbar[v] - Fv[v];
+    }
   };
   const int irows = icnt[1] * icnt[2];
   parallel_for(irows, nthreads, [&](int row) {
@@ -742,6 +803,11 @@ int slab_rhs(const kfvm_table* t, const Consts& k, const Slab& S, double* out, i
         acc = acc + (Fhi[1][v] - Flo[1][v]);
         if (dim == 3) acc = acc + (Fhi[2][v] - Flo[2][v]);
         o[v] = -(acc / k.dx);
+      }
+      if (k.g2 != 0.0) {  // gravity source from the cell average (P eq rtSource)
+        const double* U = S.at(i, j, kk);
+        o[2] = o[2] + k.g2 * U[0];
+        o[nv - 1] = o[nv - 1] + k.g2 * U[2];
       }
     }
   });
@@ -868,6 +934,17 @@ int kfo_states(const kfvm_config* cfg, const kfvm_table* t, const double* U, dou
   std::vector<uint8_t> fl;
   if (k.kx) fl = global_flags(t, k, U, nthreads);
   return slab_rhs(t, k, S, tmp.data(), nthreads, states, k.kx ? fl.data() : nullptr);
+}
+
+// Viscous flux F^(v) of one face (S:571-580 examples): the face between the
+// global cells (i,j,k) - e_d and (i,j,k) of the global AoS state U.
+void kfo_viscous_face(const kfvm_config* cfg, const double* U, int i, int j, int kk, int d,
+                      double* Fv) {
+  const Consts k = make_consts(cfg, nullptr);
+  Slab S;
+  S.init(k, 0, k.n[k.dim - 1]);
+  S.load(U);
+  viscous_flux(k, S, d, i, j, kk, Fv);
 }
 
 // KXRCF flags of every cell (1 = WENO), global AoS cell order

@@ -49,6 +49,8 @@ int kfo_sample_stage(const kfvm_config* cfg, const kfvm_table* t, const double* 
 int kfo_kxrcf_flags(const kfvm_config* cfg, const kfvm_table* t, const double* U,
                     unsigned char* flags, int nthreads);
 double kfo_pow(double x, double y);
+void kfo_viscous_face(const kfvm_config* cfg, const double* U, int i, int j, int k, int d,
+                      double* Fv);
 /* SSP(4,3)+SSP(3,2) stage combine, stage codes 11..14 (uhat written at 13). */
 void kfo_combine43(int stage, long long n, const double* U0, const double* Uk, const double* L,
                    double dt, double* out, double* uhat);

@@ -51,6 +51,7 @@ def lib():
             "kfo_kxrcf_flags": (I, [CF, T, P, P, I]),
             "kfo_advance43": (I, [CF, T, P, C.c_double, I, P, I, P, D, I]),
             "kfo_pow": (C.c_double, [C.c_double, C.c_double]),
+            "kfo_viscous_face": (None, [CF, P, I, I, I, I, P]),
             "kfo_combine43": (None, [I, C.c_longlong, P, P, P, C.c_double, P, P]),
         }
         for name, (res, args) in sig.items():
@@ -98,6 +99,13 @@ class Oracle:
         out = np.zeros(self.grid.shape, dtype=np.uint8)
         self._chk(self.L.kfo_kxrcf_flags(C.byref(self.cfg), self.rset.c_table, _p(U), _p(out),
                                          self.nthreads), "kxrcf_flags")
+        return out
+
+    def viscous_face(self, U, i, j, k, d):
+        """F^(v) of the face between global cells (i,j,k) - e_d and (i,j,k)."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.zeros(self.grid.nvar)
+        self.L.kfo_viscous_face(C.byref(self.cfg), _p(U), int(i), int(j), int(k), int(d), _p(out))
         return out
 
     def select_dt(self, U):

@@ -43,6 +43,8 @@ class KfvmConfig(C.Structure):
         ("kxrcf", C.c_int), ("kxrcf_m", C.c_double),
         ("integrator", C.c_int), ("atol", C.c_double), ("rtol", C.c_double),
         ("safety", C.c_double), ("dt_min", C.c_double), ("dt_max", C.c_double),
+        ("viscous", C.c_int), ("reynolds", C.c_double), ("prandtl", C.c_double),
+        ("mach", C.c_double), ("inv_froude2", C.c_double),
     ]
 
 

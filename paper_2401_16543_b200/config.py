@@ -41,6 +41,11 @@ class GridConfig:
     safety: float = 0.9
     dt_min: float = 0.0         # 0 = none
     dt_max: float = 0.0         # 0 = none
+    viscous: bool = False       # Navier-Stokes fluxes
+    reynolds: float = 1.0       # Re
+    prandtl: float = 0.71       # Pr
+    mach: float = 1.0           # Ma: T = gamma Ma^2 p / rho
+    froude: float | None = None  # gravity source 1/Fr^2 along +y (P eq rtSource); None = off
 
     def __post_init__(self):
         if self.dim not in (2, 3):
@@ -53,6 +58,10 @@ class GridConfig:
             raise ValueError("integrator must be ssprk3 or ssp43")
         if self.riemann not in ("hllc", "hll"):
             raise ValueError("riemann must be hllc or hll")
+        if self.viscous and not (self.reynolds > 0 and self.prandtl > 0 and self.mach > 0):
+            raise ValueError("viscous terms need Re, Pr, Ma > 0")
+        if self.froude is not None and not self.froude > 0:
+            raise ValueError("froude must be positive")
         if min(self.nx, self.ny, self.nz) < 1:
             raise ValueError("grid extents must be positive")
 
@@ -85,6 +94,9 @@ class GridConfig:
         c.integrator = 1 if self.integrator == "ssp43" else 0
         c.atol, c.rtol, c.safety = self.atol, self.rtol, self.safety
         c.dt_min, c.dt_max = self.dt_min, self.dt_max
+        c.viscous = int(bool(self.viscous))
+        c.reynolds, c.prandtl, c.mach = float(self.reynolds), float(self.prandtl), float(self.mach)
+        c.inv_froude2 = 0.0 if self.froude is None else 1.0 / (float(self.froude) * float(self.froude))
         return c
 
 

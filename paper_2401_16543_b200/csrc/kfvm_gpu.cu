@@ -174,6 +174,85 @@ __global__ void __launch_bounds__(128) k_flux_edges(const double* __restrict__ S
   }
 }
 
+// ---------------------------------------------------------------- k_visc
+// Viscous face flux (PAPER.md eqs nsVisc/shearTensor/thermalFlux,
+// P:615-633), one thread per (face, direction) over k_flux's face box:
+// F -= F^(v) with F^(v) from second-order differences of the cell-average
+// primitives (k_prims' u_d, and T = gamma Ma^2 p (1/rho)), the same
+// operations as the oracle's viscous_flux.
+template <int DIM>
+__device__ __forceinline__ void visc_prim(const double* __restrict__ Pr, long long vs, long long i,
+                                          double* o) {
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) o[a] = Pr[(3 + a) * vs + i];
+  o[DIM] = c_k.gmm * (Pr[i] * Pr[2 * vs + i]);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(128) k_visc(const double* __restrict__ Pr, double* __restrict__ F,
+                                              Geo g, Chunk ch) {
+  constexpr int nv = DIM + 2;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= ch.nfb) return;
+  const int d = blockIdx.y;
+  const int a = (int)(tid % ch.fx);
+  const long long r1 = tid / ch.fx;
+  const int b = (int)(r1 % ch.fm);
+  const int c = (int)(r1 / ch.fm);
+  const int nm = DIM == 3 ? g.nm : 1;
+  const bool slab = d == DIM - 1;
+  const bool mid = DIM == 3 && d == 1;
+  const bool valid = (d == 0 ? true : a < g.nx) && (mid ? true : (DIM == 3 ? b < nm : true)) &&
+                     (slab ? true : c < ch.C);
+  if (!valid) return;
+  // right cell (x, j, p) in local coordinates; left = right - e_d
+  int cR[3] = {a, DIM == 3 ? b : 0, ch.c0 + c};
+  int cL[3] = {cR[0], cR[1], cR[2]};
+  const int ax = d == 0 ? 0 : (slab ? 2 : 1);  // storage axis of the normal
+  cL[ax] -= 1;
+  const long long vs = g.vstride;
+  double L[4], R[4];
+  visc_prim<DIM>(Pr, vs, uidx<DIM>(g, cL[0], cL[1], cL[2]), L);
+  visc_prim<DIM>(Pr, vs, uidx<DIM>(g, cR[0], cR[1], cR[2]), R);
+  double gr[4][3];  // gr[f][t]: d phi_f / d x_t (t = physical axis)
+#pragma unroll
+  for (int f = 0; f <= DIM; ++f) gr[f][d] = (R[f] - L[f]) / c_k.dx;
+#pragma unroll
+  for (int t = 0; t < DIM; ++t) {
+    if (t == d) continue;
+    const int tx = t == 0 ? 0 : (t == DIM - 1 ? 2 : 1);
+    int o[3] = {0, 0, 0};
+    o[tx] = 1;
+    double Lp[4], Lm[4], Rp[4], Rm[4];
+    visc_prim<DIM>(Pr, vs, uidx<DIM>(g, cL[0] + o[0], cL[1] + o[1], cL[2] + o[2]), Lp);
+    visc_prim<DIM>(Pr, vs, uidx<DIM>(g, cL[0] - o[0], cL[1] - o[1], cL[2] - o[2]), Lm);
+    visc_prim<DIM>(Pr, vs, uidx<DIM>(g, cR[0] + o[0], cR[1] + o[1], cR[2] + o[2]), Rp);
+    visc_prim<DIM>(Pr, vs, uidx<DIM>(g, cR[0] - o[0], cR[1] - o[1], cR[2] - o[2]), Rm);
+#pragma unroll
+    for (int f = 0; f <= DIM; ++f) gr[f][t] = ((Lp[f] - Lm[f]) + (Rp[f] - Rm[f])) / (4.0 * c_k.dx);
+  }
+  double div = gr[0][0];
+#pragma unroll
+  for (int t = 1; t < DIM; ++t) div = div + gr[t][t];
+  double sig[3];
+#pragma unroll
+  for (int t = 0; t < DIM; ++t) {
+    double s = gr[t][d] + gr[d][t];
+    if (t == d) s = fma(-2.0 / 3.0, div, s);
+    sig[t] = s * c_k.inv_re;
+  }
+  double e = gr[DIM][d] * c_k.inv_prre;
+#pragma unroll
+  for (int t = 0; t < DIM; ++t) e = fma(sig[t], 0.5 * (L[t] + R[t]), e);
+#pragma unroll
+  for (int t = 0; t < DIM; ++t) {
+    double* q = F + (long long)(d * nv + 1 + t) * ch.nfb + tid;
+    *q = *q - sig[t];
+  }
+  double* q = F + (long long)(d * nv + nv - 1) * ch.nfb + tid;
+  *q = *q - e;
+}
+
 #include "kfvm_kxrcf.cuh"
 
 // max of non-negative doubles through their bit patterns (exact, order-free):
@@ -191,7 +270,7 @@ __device__ __forceinline__ void warp_max_atomic(unsigned long long* dst, double 
 
 // ---------------------------------------------------------------- k_update
 // mode 0: write L(u) into Uout; mode 1..3: SSP-RK3 stage combine.
-template <int DIM>
+template <int DIM, bool GRAV = false>
 __global__ void __launch_bounds__(256) k_update(const double* __restrict__ F,
                                                 const double* __restrict__ U0,
                                                 const double* __restrict__ Uk,
@@ -228,7 +307,11 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ F,
     acc = acc + (F[(long long)(1 * nv + v) * ch.nfb + fh[1]] - F[(long long)(1 * nv + v) * ch.nfb + f0]);
     if (DIM == 3)
       acc = acc + (F[(long long)(2 * nv + v) * ch.nfb + fh[2]] - F[(long long)(2 * nv + v) * ch.nfb + f0]);
-    const double L = -(acc / c_k.dx);
+    double L = -(acc / c_k.dx);
+    if (GRAV) {  // gravity source from the cell average (P eq rtSource)
+      if (v == 2) L = L + c_k.g2 * Uk[ou];
+      if (v == nv - 1) L = L + c_k.g2 * Uk[2 * g.vstride + ou];
+    }
     if (stage == 0) {
       un[v] = L;
     } else if (stage > 10) {
@@ -458,6 +541,8 @@ struct kfvm_handle {
   bool fast = true;
   int engine = 2;  // 0 generic (k_states), 1 unrolled DFMA (k_states_fast), 2 tensor core (k_states_u)
   int kz = 16;     // planes marched by one k_states_u CTA
+  bool visc = false;  // Navier-Stokes fluxes (k_visc after the face fluxes)
+  bool grav = false;  // gravity source in k_update
   double *d_Bd = nullptr, *d_Bf = nullptr;
   int* d_gat4 = nullptr;
   cudaEvent_t ev[2];
@@ -659,11 +744,22 @@ void states_only(kfvm_handle* h, const double* U, const Chunk& ch) {
 bool fused_engine(const kfvm_handle* h) { return h->dim == 2 && h->engine == 3 && !h->kx; }
 
 void flux_only(kfvm_handle* h, const Chunk& ch) {
-  if (fused_engine(h)) return;
-  if (h->dim == 2 && h->R == 2) launch_flux<2, 2>(h, ch);
-  if (h->dim == 2 && h->R == 3) launch_flux<2, 3>(h, ch);
-  if (h->dim == 3 && h->R == 2) launch_flux<3, 2>(h, ch);
-  if (h->dim == 3 && h->R == 3) launch_flux<3, 3>(h, ch);
+  if (!fused_engine(h)) {
+    if (h->dim == 2 && h->R == 2) launch_flux<2, 2>(h, ch);
+    if (h->dim == 2 && h->R == 3) launch_flux<2, 3>(h, ch);
+    if (h->dim == 3 && h->R == 2) launch_flux<3, 2>(h, ch);
+    if (h->dim == 3 && h->R == 3) launch_flux<3, 3>(h, ch);
+  }
+  if (h->visc) {  // F -= F^(v) on the same faces (needs the stage's k_prims)
+    tic(h);
+    if (h->dim == 2)
+      k_visc<2><<<dim3((unsigned)blocks(ch.nfb, 128), 2), 128, 0, h->stream>>>(h->Pr, h->F, h->g, ch);
+    else
+      k_visc<3><<<dim3((unsigned)blocks(ch.nfb, 128), 3), 128, 0, h->stream>>>(h->Pr, h->F, h->g, ch);
+    dbg_sync(h, "k_visc");
+    h->launches++;
+    toc(h, &h->t_flux);
+  }
 }
 
 void states_and_flux(kfvm_handle* h, const double* U, const Chunk& ch) {
@@ -677,12 +773,18 @@ void update(kfvm_handle* h, const Chunk& ch, const double* U0, const double* Uk,
   tic(h);
   unsigned long long* sm = stage == 3 ? h->d_smax : nullptr;
   double* uh = stage == 13 ? h->Uh : nullptr;
-  if (h->dim == 2)
+  if (h->dim == 2 && !h->grav)
     k_update<2><<<blocks(n, 256), 256, 0, h->stream>>>(h->F, U0, Uk, Uout, h->g, ch, stage,
                                                        h->d_dt_cur, sm, h->d_err, uh);
-  else
+  else if (h->dim == 2)
+    k_update<2, true><<<blocks(n, 256), 256, 0, h->stream>>>(h->F, U0, Uk, Uout, h->g, ch, stage,
+                                                             h->d_dt_cur, sm, h->d_err, uh);
+  else if (!h->grav)
     k_update<3><<<blocks(n, 256), 256, 0, h->stream>>>(h->F, U0, Uk, Uout, h->g, ch, stage,
                                                        h->d_dt_cur, sm, h->d_err, uh);
+  else
+    k_update<3, true><<<blocks(n, 256), 256, 0, h->stream>>>(h->F, U0, Uk, Uout, h->g, ch, stage,
+                                                             h->d_dt_cur, sm, h->d_err, uh);
   h->launches++;
   toc(h, &h->t_update);
 }
@@ -1192,6 +1294,9 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
       (cfg->bc != KFVM_BC_PERIODIC && cfg->bc != KFVM_BC_OUTFLOW) ||
       (cfg->riemann != KFVM_RIEMANN_HLLC && cfg->riemann != KFVM_RIEMANN_HLL))
     return KFVM_ERR_CONFIG;
+  if (cfg->viscous && !(cfg->reynolds > 0 && cfg->prandtl > 0 && cfg->mach > 0))
+    return KFVM_ERR_CONFIG;  // the viscous terms need Re, Pr, Ma
+  if (!std::isfinite(cfg->inv_froude2)) return KFVM_ERR_CONFIG;
   kfvm_handle* h = new kfvm_handle();
   h->cfg = *cfg;
   h->dim = cfg->dim;
@@ -1256,6 +1361,13 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   k.dt_min = cfg->dt_min;
   k.dt_max = cfg->dt_max > 0.0 ? cfg->dt_max : INFINITY;
   h->integrator = cfg->integrator;
+  k.visc = cfg->viscous ? 1 : 0;
+  k.inv_re = 1.0 / cfg->reynolds;  // the oracle computes the same doubles
+  k.inv_prre = 1.0 / (cfg->prandtl * cfg->reynolds);
+  k.gmm = cfg->gamma * (cfg->mach * cfg->mach);
+  k.g2 = cfg->inv_froude2;
+  h->visc = cfg->viscous != 0;
+  h->grav = cfg->inv_froude2 != 0.0;
   k.kx = cfg->kxrcf ? 1 : 0;
   k.dm = std::pow(cfg->dx, cfg->kxrcf_m);  // the oracle computes the same std::pow
   h->kx = cfg->kxrcf != 0;

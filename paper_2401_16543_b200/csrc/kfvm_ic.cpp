@@ -271,6 +271,11 @@ extern "C" void kfvm_config_defaults(kfvm_config* c, int dim, int radius, int nx
   c->safety = 0.9;
   c->dt_min = 0.0;
   c->dt_max = 0.0;
+  c->viscous = 0;
+  c->reynolds = 1.0;
+  c->prandtl = 0.71;
+  c->mach = 1.0;
+  c->inv_froude2 = 0.0;
 }
 
 extern "C" void kfvm_slab_range(int n_global, int nranks, int rank, int* p0, int* np) {

@@ -53,6 +53,11 @@ def test_config_errors_without_gpu():
     L.kfvm_config_defaults(C.byref(bad), 3, 2, 16, 16, 16, 0)  # dim 3 vs 2-D table
     h = C.c_void_p()
     assert L.kfvm_gpu_create(C.byref(bad), p, None, C.byref(h)) == _abi.KFVM_ERR_CONFIG
+    visc = _abi.KfvmConfig()
+    L.kfvm_config_defaults(C.byref(visc), 2, 2, 16, 16, 1, 0)
+    assert visc.viscous == 0 and visc.prandtl == 0.71 and visc.inv_froude2 == 0.0
+    visc.viscous, visc.reynolds = 1, 0.0  # Re must be positive
+    assert L.kfvm_gpu_create(C.byref(visc), p, None, C.byref(h)) == _abi.KFVM_ERR_CONFIG
     L.kfvm_table_free(p)
 
 
