@@ -40,9 +40,15 @@ __constant__ DevConsts c_k;
 __constant__ DevTable c_t;
 __constant__ int c_gather[512];
 
+// Storage: [var][plane][mid][x] with ghost cells: H halo planes on the slab
+// axis, G = H ghost columns in x and Gm (= H in 3-D, 0 in 2-D) ghost rows in
+// the mid axis, filled every stage (k_ghost per boundary kind, then the
+// slab-axis halo exchange of whole padded planes), so every gather is affine.
 struct Geo {
   int nx, nm, np_loc, H;  // x extent, mid extent (1 in 2-D), local slab planes, halo
-  long long pstride;      // elements per slab-axis plane
+  int G, Gm, nxp;         // ghost columns, ghost rows, padded row length
+  int xo;                 // offset of cell x = 0 in a row (>= G, 128-byte aligned)
+  long long pstride;      // elements per slab-axis plane: nxp (nm + 2Gm)
   long long vstride;      // elements per variable
 };
 
@@ -69,10 +75,13 @@ __device__ __forceinline__ int remap(int i, int n, int bc) {
   return i < 0 ? 0 : (i >= n ? n - 1 : i);
 }
 
+// padded-storage offsets of x, mid row j, local plane p (ghosts included)
+__device__ __forceinline__ int xoff(const Geo& g, int x) { return x + g.xo; }
+__device__ __forceinline__ long long moff(const Geo& g, int j) { return (long long)(j + g.Gm) * g.nxp; }
 template <int DIM>
 __device__ __forceinline__ long long uidx(const Geo& g, int x, int j, int p) {
-  long long o = (long long)(p + g.H) * g.pstride + remap(x, g.nx, c_k.bc);
-  if (DIM == 3) o += (long long)remap(j, g.nm, c_k.bc) * g.nx;
+  long long o = (long long)(p + g.H) * g.pstride + xoff(g, x);
+  if (DIM == 3) o += moff(g, j);
   return o;
 }
 
@@ -298,7 +307,7 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ F,
   } else {
     fh[1] = f0 + (long long)ch.fm * ch.fx;
   }
-  const long long ou = (long long)(ch.c0 + c + g.H) * g.pstride + (long long)b * g.nx + a;
+  const long long ou = uidx<DIM>(g, a, b, ch.c0 + c);
   const double dt = stage ? *dtp : 0.0;
   double un[nv];
 #pragma unroll
@@ -337,7 +346,9 @@ __global__ void k_speed(const double* __restrict__ U, Geo g, unsigned long long*
   const long long ncell = (long long)g.nx * nm * g.np_loc;
   const long long tid0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long tid = tid0 < ncell ? tid0 : ncell - 1;
-  const long long ou = (long long)g.H * g.pstride + tid;
+  const int a = (int)(tid % g.nx);
+  const long long r1 = tid / g.nx;
+  const long long ou = uidx<DIM>(g, a, (int)(r1 % nm), (int)(r1 / nm));
   double u[nv];
 #pragma unroll
   for (int v = 0; v < nv; ++v) u[v] = U[v * g.vstride + ou];
@@ -388,15 +399,61 @@ __global__ void k_halo_local(double* __restrict__ U, Geo g, int nv, int nglob, i
       U[v * g.vstride + (long long)(src + g.H) * g.pstride + o];
 }
 
+// Ghost cells (fill_ghost) in one launch: every ghost cell of the
+// padded local block — the x ghost columns and mid ghost rows of the planes
+// [-hp, np + hp) and, with hp = H (one rank), the interior block of the
+// slab-axis halo planes — gets the value of the cell its boundary kinds map
+// to, the maps composed over the axes (periodic wrap / outflow clamp).  With
+// several ranks (hp = 0) the halo planes are exchanged afterwards as whole
+// padded planes.
+__global__ void k_ghost(double* __restrict__ U, Geo g, int nv, int nsa, int hp) {
+  const int P = g.np_loc + 2 * hp, rows = g.nm + 2 * g.Gm;
+  const long long nA = 2LL * g.G * rows * P, nB = 2LL * g.Gm * g.nx * P,
+                  nC = 2LL * hp * g.nm * g.nx, n = nA + nB + nC;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * nv) return;
+  const int v = (int)(t / n);
+  long long e = t % n;
+  int x, j, p;
+  if (e < nA) {  // x ghost columns, every row and plane
+    const int gi = (int)(e % (2 * g.G));
+    e /= 2 * g.G;
+    x = gi < g.G ? gi - g.G : g.nx + gi - g.G;
+    j = (int)(e % rows) - g.Gm;
+    p = (int)(e / rows) - hp;
+  } else if ((e -= nA) < nB) {  // mid ghost rows, interior columns
+    x = (int)(e % g.nx);
+    e /= g.nx;
+    const int gj = (int)(e % (2 * g.Gm));
+    j = gj < g.Gm ? gj - g.Gm : g.nm + gj - g.Gm;
+    p = (int)(e / (2 * g.Gm)) - hp;
+  } else {  // halo planes, interior block
+    e -= nB;
+    x = (int)(e % g.nx);
+    e /= g.nx;
+    j = (int)(e % g.nm);
+    const int l = (int)(e / g.nm);
+    p = l < hp ? l - hp : g.np_loc + l - hp;
+  }
+  const int xs = remap(x, g.nx, c_k.bc);
+  const int js = g.Gm ? remap(j, g.nm, c_k.bc) : j;
+  const int ps = hp ? remap(p, nsa, c_k.bc) : p;
+  const long long vb = v * g.vstride;
+  U[vb + (long long)(p + g.H) * g.pstride + moff(g, j) + xoff(g, x)] =
+      U[vb + (long long)(ps + g.H) * g.pstride + moff(g, js) + xoff(g, xs)];
+}
+
 // AoS (host order) <-> SoA interior planes
 template <int DIR>
 __global__ void k_transpose(double* __restrict__ soa, double* __restrict__ aos, Geo g, int nv) {
-  const long long n = (long long)g.pstride * g.np_loc;
+  const long long n = (long long)g.nx * g.nm * g.np_loc;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= n * nv) return;
   const long long c = tid / nv;
   const int v = (int)(tid % nv);
-  const long long o = (long long)g.H * g.pstride + c;
+  const long long r1 = c / g.nx;
+  const long long o = (long long)((int)(r1 / g.nm) + g.H) * g.pstride + moff(g, (int)(r1 % g.nm)) +
+                      xoff(g, (int)(c % g.nx));
   if (DIR == 0)
     soa[v * g.vstride + o] = aos[tid];
   else
@@ -450,7 +507,7 @@ __global__ void k_ic_fill(const ICPlan* P, double* U, Geo g, int p0) {
     cell_average(*P, i, b, p0 + pl, out);
   else
     cell_average(*P, i, p0 + pl, 0, out);
-  const long long o = (long long)(pl + g.H) * g.pstride + (long long)b * g.nx + i;
+  const long long o = (long long)(pl + g.H) * g.pstride + moff(g, b) + xoff(g, i);
   for (int v = 0; v < P->dim + 2; ++v) U[v * g.vstride + o] = out[v];
 }
 
@@ -789,13 +846,24 @@ void update(kfvm_handle* h, const Chunk& ch, const double* U0, const double* Uk,
   toc(h, &h->t_update);
 }
 
+// ghost cells of the local block (one rank: the halo planes too)
+void ghost(kfvm_handle* h, double* U) {
+  const Geo& g = h->g;
+  const int hp = h->nranks == 1 ? g.H : 0, P = g.np_loc + 2 * hp;
+  const long long n = 2LL * g.G * (g.nm + 2 * g.Gm) * P + 2LL * g.Gm * g.nx * P +
+                      2LL * hp * g.nm * g.nx;
+  tic(h);
+  k_ghost<<<blocks(n * h->nv, 256), 256, 0, h->stream>>>(U, g, h->nv, h->nsa, hp);
+  h->launches++;
+  toc(h, &h->t_other);
+}
+
 // fill the slab-axis halo planes of U (local copy and/or NCCL exchange)
 int halo(kfvm_handle* h, double* U, cudaStream_t st) {
   const long long per = (long long)h->g.H * h->g.pstride;
   tic(h);
   if (h->nranks == 1) {
-    k_halo_local<<<blocks(2 * per * h->nv, 256), 256, 0, st>>>(U, h->g, h->nv, h->nsa, 3);
-    h->launches++;
+    (void)per;  // k_ghost filled the halo planes
   } else {
     NcclApi& N = nccl();
     const bool periodic = h->cfg.bc == KFVM_BC_PERIODIC;
@@ -921,6 +989,7 @@ int kx_flags(kfvm_handle* h, const double* U, const Chunk& ch) {
 int run_stage(kfvm_handle* h, const double* Uin, double* Uout, int stage) {
   const int np = h->g.np_loc, R = h->R;
   if (h->kx) {  // single chunk (checked at create)
+    ghost(h, const_cast<double*>(Uin));
     int rc = halo(h, const_cast<double*>(Uin), h->stream);
     if (rc) return rc;
     prims(h, Uin);
@@ -937,12 +1006,14 @@ int run_stage(kfvm_handle* h, const double* Uin, double* Uout, int stage) {
   const int nch = (np + h->chunk - 1) / h->chunk;
   auto needs_halo = [&](int c0, int C) { return c0 - 1 - R < 0 || c0 + C + R > np - 1; };
   if (!h->overlap || fused_engine(h) || np < 2 * R + 3) {
+    ghost(h, const_cast<double*>(Uin));
     int rc = halo(h, const_cast<double*>(Uin), h->stream);
     if (rc) return rc;
     prims(h, Uin);
     run_planes(h, Uin, Uout, stage, 0, np);
     return KFVM_OK;
   }
+  ghost(h, const_cast<double*>(Uin));
   CK(cudaEventRecord(h->ev_fork, h->stream));
   CK(cudaStreamWaitEvent(h->s_halo, h->ev_fork, 0));
   int rc = halo(h, const_cast<double*>(Uin), h->s_halo);
@@ -1023,7 +1094,7 @@ __global__ void k_err_rows(const double* __restrict__ Up, const double* __restri
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)nrow * g.np_loc) return;
   const int j = (int)(t % nrow), p = (int)(t / nrow);
-  const long long base = (long long)(p + g.H) * g.pstride + (long long)j * g.nx;
+  const long long base = (long long)(p + g.H) * g.pstride + moff(g, j) + xoff(g, 0);
   double r = 0.0;
   for (int x = 0; x < g.nx; ++x)
 #pragma unroll
@@ -1185,8 +1256,13 @@ int ensure_dt_cap(kfvm_handle* h, int n) {
   return KFVM_OK;
 }
 
+// interior cells x variables of the rank (the AoS host / staging layout)
+long long interior_elems(const kfvm_handle* h) {
+  return (long long)h->g.nx * h->g.nm * h->g.np_loc * h->nv;
+}
+
 int ensure_aos(kfvm_handle* h) {
-  const size_t n = (size_t)h->g.pstride * h->g.np_loc * h->nv;
+  const size_t n = (size_t)interior_elems(h);
   if (h->aos_elems >= n) return KFVM_OK;
   if (h->aos) cudaFree(h->aos);
   CK(cudaMalloc(&h->aos, n * sizeof(double)));
@@ -1331,7 +1407,13 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     delete h;
     return fail(nullptr, KFVM_ERR_CONFIG, "slab thinner than the halo");
   }
-  h->g.pstride = (long long)h->g.nx * h->g.nm;
+  h->g.G = h->g.H;
+  h->g.Gm = cfg->dim == 3 ? h->g.H : 0;
+  // rows start 128-byte aligned and cell 0 sits at a 128-byte boundary, so
+  // the engines' 32-cell segments keep the alignment of an unpadded row
+  h->g.xo = 16;
+  h->g.nxp = (h->g.xo + h->g.nx + h->g.G + 15) / 16 * 16;
+  h->g.pstride = (long long)h->g.nxp * (h->g.nm + 2 * h->g.Gm);
   h->g.vstride = h->g.pstride * (np + 2 * h->g.H);
   // constants (pinned on the host once)
   DevConsts& k = h->kc;
@@ -1548,7 +1630,7 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
 }
 
 extern "C" int kfvm_gpu_set_state_device(kfvm_handle* h, const double* U_dev) {
-  const long long n = h->g.pstride * h->g.np_loc * h->nv;
+  const long long n = interior_elems(h);
   k_transpose<0><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, const_cast<double*>(U_dev), h->g,
                                                          h->nv);
   h->launches++;
@@ -1559,7 +1641,7 @@ extern "C" int kfvm_gpu_set_state_device(kfvm_handle* h, const double* U_dev) {
 }
 
 extern "C" int kfvm_gpu_get_state_device(kfvm_handle* h, double* U_dev) {
-  const long long n = h->g.pstride * h->g.np_loc * h->nv;
+  const long long n = interior_elems(h);
   k_transpose<1><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, U_dev, h->g, h->nv);
   h->launches++;
   CK(cudaStreamSynchronize(h->stream));
@@ -1569,7 +1651,7 @@ extern "C" int kfvm_gpu_get_state_device(kfvm_handle* h, double* U_dev) {
 extern "C" int kfvm_gpu_set_state(kfvm_handle* h, const double* U_host) {
   int rc = ensure_aos(h);
   if (rc) return rc;
-  const size_t n = (size_t)h->g.pstride * h->g.np_loc * h->nv;
+  const size_t n = (size_t)interior_elems(h);
   CK(cudaMemcpyAsync(h->aos, U_host, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   return kfvm_gpu_set_state_device(h, h->aos);
 }
@@ -1579,7 +1661,7 @@ extern "C" int kfvm_gpu_get_state(kfvm_handle* h, double* U_host) {
   if (rc) return rc;
   rc = kfvm_gpu_get_state_device(h, h->aos);
   if (rc) return rc;
-  const size_t n = (size_t)h->g.pstride * h->g.np_loc * h->nv;
+  const size_t n = (size_t)interior_elems(h);
   CK(cudaMemcpyAsync(U_host, h->aos, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return KFVM_OK;
@@ -1590,7 +1672,7 @@ extern "C" int kfvm_gpu_rhs(kfvm_handle* h, double* dUdt_host) {
   if (rc) return rc;
   if ((rc = check_err(h))) return rc;
   if ((rc = ensure_aos(h))) return rc;
-  const long long n = h->g.pstride * h->g.np_loc * h->nv;
+  const long long n = interior_elems(h);
   k_transpose<1><<<blocks(n, 256), 256, 0, h->stream>>>(h->Ua, h->aos, h->g, h->nv);
   h->launches++;
   CK(cudaMemcpyAsync(dUdt_host, h->aos, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1599,11 +1681,12 @@ extern "C" int kfvm_gpu_rhs(kfvm_handle* h, double* dUdt_host) {
 }
 
 extern "C" int kfvm_gpu_states(kfvm_handle* h, double* states_host) {
+  ghost(h, h->U0);
   int rc = halo(h, h->U0, h->stream);
   if (rc) return rc;
   prims(h, h->U0);
   const long long per_cell = (long long)h->NP * h->nv;
-  const long long plane_cells = h->g.pstride;
+  const long long plane_cells = (long long)h->g.nx * h->g.nm;  // interior cells per plane
   double* dbuf = nullptr;
   CK(cudaMalloc(&dbuf, (size_t)plane_cells * h->chunk * per_cell * sizeof(double)));
   for (int c0 = 0; c0 < h->g.np_loc; c0 += h->chunk) {
@@ -1639,6 +1722,7 @@ __global__ void k_extract_flags(const unsigned char* __restrict__ fl, unsigned c
 
 extern "C" int kfvm_gpu_kxrcf_flags(kfvm_handle* h, unsigned char* flags_host) {
   if (!h->kx) return fail(h, KFVM_ERR_CONFIG, "kxrcf is off in this handle's config");
+  ghost(h, h->U0);
   int rc = halo(h, h->U0, h->stream);
   if (rc) return rc;
   prims(h, h->U0);

@@ -85,13 +85,13 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
   for (int k = 0; k < NLU; ++k) {
     const int i = threadIdx.x + 128 * k;
     const int rx = i % C::RX, v = i / C::RX;
-    offU[k] = i < C::PL ? (unsigned)(v * g.vstride + remap(x0 - R + rx, g.nx, c_k.bc)) : 0u;
+    offU[k] = i < C::PL ? (unsigned)(v * g.vstride + xoff(g, x0 - R + rx)) : 0u;
   }
 #pragma unroll
   for (int k = 0; k < NLP; ++k) {
     const int i = threadIdx.x + 128 * k;
     const int rx = i % C::NX, f = i / C::NX;
-    offP[k] = i < C::PPL ? (unsigned)(f * g.vstride + remap(x0 - 1 + rx, g.nx, c_k.bc)) : 0u;
+    offP[k] = i < C::PPL ? (unsigned)(f * g.vstride + xoff(g, x0 - 1 + rx)) : 0u;
   }
   auto load_row = [&](int p) {
     double* dst = sRing + ((p + 4 * C::RING) % C::RING) * C::PL;

@@ -145,9 +145,9 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     for (int i = threadIdx.x; i < C::PL; i += 128) {
       const int rx = i % C::RX, rr = i / C::RX;
       const int ry = rr % C::RY, v = rr / C::RY;
-      const int xx = remap(x0 - R + rx, g.nx, c_k.bc);
+      const int xx = xoff(g, x0 - R + rx);
       const long long off = v * g.vstride + pbase + xx +
-                            (D == 3 ? (long long)remap(j - R + ry, g.nm, c_k.bc) * g.nx : 0);
+                            (D == 3 ? moff(g, j - R + ry) : 0);
       __pipeline_memcpy_async(dst + i, U + off, sizeof(double));
     }
   };
@@ -157,9 +157,9 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     for (int i = threadIdx.x; i < C::PPL; i += 128) {
       const int rx = i % C::NX, rr = i / C::NX;
       const int ry = rr % C::NY, f = rr / C::NY;
-      const int xx = remap(x0 - 1 + rx, g.nx, c_k.bc);
+      const int xx = xoff(g, x0 - 1 + rx);
       const long long off = f * g.vstride + pbase + xx +
-                            (D == 3 ? (long long)remap(j - 1 + ry, g.nm, c_k.bc) * g.nx : 0);
+                            (D == 3 ? moff(g, j - 1 + ry) : 0);
       __pipeline_memcpy_async(dst + i, Pr + off, sizeof(double));
     }
   };
