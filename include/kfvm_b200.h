@@ -43,8 +43,23 @@ extern "C" {
 #define KFVM_ERR_RUNTIME 2
 #define KFVM_ERR_DEVICE 3
 
+/* Boundary kinds (BoundaryKind; fill_ghost).  Every
+ * kind defines the value of every ghost cell (an infinite extension, so the
+ * ghost cells' own reconstructions give the exterior face states):
+ *   PERIODIC   wrap (sides come in pairs)
+ *   OUTFLOW    zeroth-order extrapolation: the nearest interior cell
+ *   REFLECTING mirror image across the wall, wall-normal momentum negated
+ *   DIRICHLET  the fixed conservative state bc_state[side]
+ *   SLIT       "user" inflow of S:561 / P:§6.4: bc_state[side] where the
+ *              ghost cell centre lies strictly inside the slit (r^2 < radius^2
+ *              in the side's tangential axes), outflow elsewhere
+ * At edges and corners the per-axis maps compose in axis order x, y, z:
+ * value = T_z(T_y(T_x(U[src]))), src the composed index map. */
 #define KFVM_BC_PERIODIC 0
 #define KFVM_BC_OUTFLOW 1
+#define KFVM_BC_REFLECTING 2
+#define KFVM_BC_DIRICHLET 3
+#define KFVM_BC_SLIT 4
 
 #define KFVM_RIEMANN_HLLC 0
 #define KFVM_RIEMANN_HLL 1
@@ -98,7 +113,8 @@ typedef struct kfvm_config {
   int dim;            /* 2 or 3 */
   int radius;         /* 2 or 3 */
   int nx, ny, nz;     /* global interior cells; nz = 1 in 2-D */
-  int bc;             /* KFVM_BC_PERIODIC or KFVM_BC_OUTFLOW, all sides */
+  int bc;             /* KFVM_BC_PERIODIC or KFVM_BC_OUTFLOW: every side, unless
+                         bc_per_side is set */
   int riemann;        /* KFVM_RIEMANN_HLLC (default) or KFVM_RIEMANN_HLL */
   double dx;          /* uniform spacing Delta (dx = dy = dz) */
   double gamma;       /* ratio of specific heats */
@@ -131,6 +147,18 @@ typedef struct kfvm_config {
    * S = (1/Fr^2) (0, 0, rho, [0,] rho u_2) from the cell averages, added to
    * the flux divergence.  0 = no source. */
   double inv_froude2;
+  /* Per-side boundary kinds (Field's "registered boundary kinds per side",
+   * S:531).  Side 2*a + s: axis a = 0 (x), 1 (y), 2 (z); s = 0 low, 1 high.
+   * bc_per_side = 0 (kfvm_config_defaults, or a zeroed struct): every side
+   * takes `bc`, the arrays below are ignored. */
+  int bc_per_side;
+  int bc_side[6];           /* KFVM_BC_* per side */
+  double bc_state[6][5];    /* DIRICHLET / SLIT inflow state, conservative
+                               (rho, m_1..m_d, E); unused entries ignored */
+  double slit_center[6][2]; /* SLIT: centre in the side's tangential axes
+                               (increasing axis order), measured from the
+                               domain's low corner */
+  double slit_radius[6];    /* SLIT: inflow where r^2 < radius^2 */
 } kfvm_config;
 
 #define KFVM_SSPRK3 0

@@ -41,6 +41,10 @@ struct Consts {
   double atol, rtol, safety, dt_min, dt_max;  // SSP(4,3) controller
   int visc;                                    // Navier-Stokes terms
   double inv_re, inv_prre, gmm, g2;            // 1/Re, 1/(Pr Re), gamma Ma^2, 1/Fr^2
+  int side[6], per[3];  // boundary kind per side 2a+s, periodic axes
+  double bst[6][5];     // dirichlet / slit inflow states
+  double slc[6][2];     // slit centres in the side's tangential axes
+  double slr2[6];       // slit radius^2
 };
 
 Consts make_consts(const kfvm_config* c, const kfvm_table* t) {
@@ -75,6 +79,17 @@ Consts make_consts(const kfvm_config* c, const kfvm_table* t) {
   k.inv_prre = 1.0 / (c->prandtl * c->reynolds);
   k.gmm = c->gamma * (c->mach * c->mach);
   k.g2 = c->inv_froude2;
+  for (int a = 0; a < 3; ++a) {
+    for (int sd = 0; sd < 2; ++sd) {
+      const int q = 2 * a + sd;
+      k.side[q] = a >= c->dim ? KFVM_BC_PERIODIC : (c->bc_per_side ? c->bc_side[q] : c->bc);
+      for (int v = 0; v < 5; ++v) k.bst[q][v] = c->bc_state[q][v];
+      k.slc[q][0] = c->slit_center[q][0];
+      k.slc[q][1] = c->slit_center[q][1];
+      k.slr2[q] = c->slit_radius[q] * c->slit_radius[q];
+    }
+    k.per[a] = k.side[2 * a] == KFVM_BC_PERIODIC ? 1 : 0;
+  }
   if (t) {
     for (int a = 0; a < t->n_alpha; ++a) {
       const int ord = t->alpha[3 * a] + t->alpha[3 * a + 1] + t->alpha[3 * a + 2];
@@ -410,17 +425,62 @@ void riemann(const Consts& k, int d, const double* UL, const double* UR, double*
 }
 
 // ------------------------------------------------------------- grid / slab
-inline int wrap(int i, int n, int bc) {
-  if (bc == KFVM_BC_PERIODIC) return ((i % n) + n) % n;
+// periodic wrap, or the nearest interior cell (the flag / index rule of the
+// one-cell ring around a box)
+inline int wrap(int i, int n, int periodic) {
+  if (periodic) return ((i % n) + n) % n;
   return i < 0 ? 0 : (i >= n ? n - 1 : i);
 }
 
+// fill_ghost: index map of one axis for a side's kind — periodic
+// wrap, reflecting mirror image, otherwise the nearest interior cell.
+inline int ghost_src(int i, int n, int kind) {
+  if (i >= 0 && i < n) return i;
+  if (kind == KFVM_BC_PERIODIC) return ((i % n) + n) % n;
+  if (kind == KFVM_BC_REFLECTING) return i < 0 ? -1 - i : 2 * n - 1 - i;
+  return i < 0 ? 0 : n - 1;
+}
+
+// fill_ghost value rule of one crossed side q = 2a+s for the ghost cell at
+// global coords c: reflecting flips the wall-normal momentum,
+// dirichlet writes the fixed state, the slit writes the inflow state where
+// r^2 < radius^2 strictly over the tangential axes' cell-centre offsets
+// (S:561), and outflow / periodic keep the source value.
+void ghost_rule(const Consts& k, int a, int sd, const int* c, double* u) {
+  const int q = 2 * a + sd;
+  switch (k.side[q]) {
+    case KFVM_BC_REFLECTING:
+      u[1 + a] = -u[1 + a];
+      break;
+    case KFVM_BC_DIRICHLET:
+      for (int v = 0; v < k.nv; ++v) u[v] = k.bst[q][v];
+      break;
+    case KFVM_BC_SLIT: {
+      double r2 = 0.0;
+      int m = 0;
+      for (int b = 0; b < k.dim; ++b) {
+        if (b == a) continue;
+        const double off = ((double)c[b] + 0.5) * k.dx - k.slc[q][m];
+        r2 = m == 0 ? off * off : r2 + off * off;
+        ++m;
+      }
+      if (r2 < k.slr2[q])
+        for (int v = 0; v < k.nv; ++v) u[v] = k.bst[q][v];
+      break;
+    }
+    default:
+      break;
+  }
+}
+
 // A slab of planes [p0, p0+np) along the slab axis sa = dim-1, stored with H
-// halo planes on each side; the other axes are remapped by the BC.
+// halo planes on each side and H ghost cells on each side of the other axes:
+// every cell of the padded box holds its value (interior copy or fill_ghost
+// rule), so at() is a plain offset.
 struct Slab {
   const Consts* k;
   int sa, p0, np, H;
-  int ext[3];  // local extents (slab axis includes halos)
+  int ext[3];  // padded local extents
   std::vector<double> U;
 
   void init(const Consts& kk, int p0_, int np_) {
@@ -429,30 +489,62 @@ struct Slab {
     p0 = p0_;
     np = np_;
     H = kk.R + 1;
-    for (int a = 0; a < 3; ++a) ext[a] = kk.n[a];
+    for (int a = 0; a < 3; ++a) ext[a] = a < kk.dim ? kk.n[a] + 2 * H : 1;
     ext[sa] = np + 2 * H;
     U.assign((size_t)ext[0] * ext[1] * ext[2] * kk.nv, 0.0);
   }
-  // global coords (i,j,k); slab axis must lie within [p0-H, p0+np+H)
+  // global coords (i,j,k) within the padded box
   inline const double* at(int i, int j, int kk) const {
     int c[3] = {i, j, kk};
-    for (int a = 0; a < k->dim; ++a) {
-      if (a == sa)
-        c[a] = c[a] - (p0 - H);
-      else
-        c[a] = wrap(c[a], k->n[a], k->bc);
-    }
+    for (int a = 0; a < k->dim; ++a) c[a] += a == sa ? H - p0 : H;
     return U.data() + (((size_t)c[2] * ext[1] + c[1]) * ext[0] + c[0]) * k->nv;
   }
-  // fill from a global AoS array: interior planes + halos (wrap/clamp of the
-  // global slab-axis index) — the in-memory halo exchange.
+  // every padded cell from src(sc), sc the composed ghost index map of its
+  // global coords, then the value rules of the crossed sides in axis order
+  // x, y, z.  A periodic slab axis is not remapped here (src resolves it:
+  // the global array wraps, a rank's halo planes hold the neighbour's data).
+  template <class Src>
+  void fill(Src&& src) {
+    const int nv = k->nv;
+    for (int l2 = 0; l2 < ext[2]; ++l2)
+      for (int l1 = 0; l1 < ext[1]; ++l1)
+        for (int l0 = 0; l0 < ext[0]; ++l0) {
+          const int l[3] = {l0, l1, l2};
+          int c[3] = {0, 0, 0}, sc[3] = {0, 0, 0};
+          for (int a = 0; a < k->dim; ++a) {
+            c[a] = l[a] - H + (a == sa ? p0 : 0);
+            const int q = 2 * a + (c[a] >= k->n[a]);
+            sc[a] = (a == sa && k->per[a]) ? c[a] : ghost_src(c[a], k->n[a], k->side[q]);
+          }
+          double u[5];
+          std::memcpy(u, src(sc), nv * sizeof(double));
+          for (int a = 0; a < k->dim; ++a)
+            if (c[a] < 0 || c[a] >= k->n[a]) ghost_rule(*k, a, c[a] >= k->n[a], c, u);
+          std::memcpy(U.data() + (((size_t)l2 * ext[1] + l1) * ext[0] + l0) * nv, u,
+                      nv * sizeof(double));
+        }
+  }
+  // from a global AoS array (the in-memory halo exchange)
   void load(const double* G) {
-    const int nsa = k->n[sa];
-    const size_t plane = (size_t)k->nv * (sa == 2 ? (size_t)k->n[0] * k->n[1] : (size_t)k->n[0]);
-    for (int lp = 0; lp < ext[sa]; ++lp) {
-      const int gp = wrap(p0 - H + lp, nsa, k->bc);
-      std::memcpy(U.data() + (size_t)lp * plane, G + (size_t)gp * plane, plane * sizeof(double));
-    }
+    const Consts& kk = *k;
+    fill([&](const int* sc) {
+      const int g = wrap(sc[sa], kk.n[sa], 1);
+      int c[3] = {sc[0], sc[1], sc[2]};
+      c[sa] = g;
+      return G + (((size_t)c[2] * kk.n[1] + c[1]) * kk.n[0] + c[0]) * kk.nv;
+    });
+  }
+  // from the slab's local AoS array with its H halo planes (interior extents
+  // in the other axes), as exchanged by the caller; planes beyond a
+  // non-periodic global end are rebuilt from the slab's own planes.
+  void load_local(const double* L) {
+    const Consts& kk = *k;
+    const size_t plane = (size_t)kk.nv * kk.n[0] * (sa == 2 ? kk.n[1] : 1);
+    fill([&](const int* sc) {
+      const int lp = sc[sa] - (p0 - H);
+      const size_t in = sa == 2 ? (size_t)sc[1] * kk.n[0] + sc[0] : (size_t)sc[0];
+      return L + (size_t)lp * plane + in * kk.nv;
+    });
   }
 };
 
@@ -593,7 +685,7 @@ std::vector<uint8_t> global_flags(const kfvm_table* t, const Consts& k, const do
           int nb[3] = {c[0], c[1], c[2]};
           nb[d] += side ? 1 : -1;
           if (nb[d] < 0 || nb[d] >= k.n[d]) {
-            if (k.bc != KFVM_BC_PERIODIC) continue;  // physical boundary face: exempt
+            if (!k.per[d]) continue;  // physical boundary face: exempt
             nb[d] = (nb[d] + k.n[d]) % k.n[d];
           }
           const size_t nid = ((size_t)nb[2] * k.n[1] + nb[1]) * k.n[0] + nb[0];
@@ -612,11 +704,11 @@ std::vector<uint8_t> global_flags(const kfvm_table* t, const Consts& k, const do
 }
 
 // flag of any cell of an extended box: global cells are their own, ghost
-// cells take the flag of the cell they replicate (periodic image / outflow
-// clamp)
+// cells take the flag of the periodic image, else of the nearest interior
+// cell (with one ghost layer that is also the reflecting mirror image)
 inline int flag_of(const Consts& k, const uint8_t* fl, int i, int j, int kk) {
-  const int c[3] = {wrap(i, k.n[0], k.bc), wrap(j, k.n[1], k.bc),
-                    k.dim == 3 ? wrap(kk, k.n[2], k.bc) : 0};
+  const int c[3] = {wrap(i, k.n[0], k.per[0]), wrap(j, k.n[1], k.per[1]),
+                    k.dim == 3 ? wrap(kk, k.n[2], k.per[2]) : 0};
   return fl[((size_t)c[2] * k.n[1] + c[1]) * k.n[0] + c[0]];
 }
 
@@ -1093,8 +1185,20 @@ int kfo_slab_rhs(const kfvm_config* cfg, const kfvm_table* t, int p0, int np,
   const Consts k = make_consts(cfg, t);
   Slab S;
   S.init(k, p0, np);
-  std::memcpy(S.U.data(), U_local, S.U.size() * sizeof(double));
+  S.load_local(U_local);
   return slab_rhs(t, k, S, out, nthreads);
+}
+
+// fill_ghost of the whole domain: out = the padded box with
+// R+1 ghost cells on every side (AoS, x fastest) — the boundary-kind hook of
+// the tests.
+int kfo_fill_ghost(const kfvm_config* cfg, const double* U, double* out) {
+  const Consts k = make_consts(cfg, nullptr);
+  Slab S;
+  S.init(k, 0, k.n[k.dim - 1]);
+  S.load(U);
+  std::memcpy(out, S.U.data(), S.U.size() * sizeof(double));
+  return 0;
 }
 
 // max over ncells AoS cells of sum_d (|u_d| + c) (the select_dt reduction)

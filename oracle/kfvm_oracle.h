@@ -58,6 +58,8 @@ void kfo_combine43(int stage, long long n, const double* U0, const double* Uk, c
 /* Slab pieces for the multi-process decomposition test. */
 int kfo_slab_rhs(const kfvm_config* cfg, const kfvm_table* t, int p0, int np,
                  const double* U_local, double* out, int nthreads);
+/* the whole domain padded with R+1 ghost cells per side by fill_ghost */
+int kfo_fill_ghost(const kfvm_config* cfg, const double* U, double* out);
 double kfo_max_speed(const kfvm_config* cfg, const double* U, long long ncells);
 void kfo_combine(int stage, long long n, const double* U0, const double* Uk, const double* L,
                  double dt, double* out);

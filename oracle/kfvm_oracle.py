@@ -37,6 +37,7 @@ def lib():
             "kfo_sample_stage": (I, [CF, T, P, I, I, I, D]),
             "kfo_slab_rhs": (I, [CF, T, I, I, P, P, I]),
             "kfo_max_speed": (C.c_double, [CF, P, C.c_longlong]),
+            "kfo_fill_ghost": (I, [CF, P, P]),
             "kfo_combine": (None, [I, C.c_longlong, P, P, P, C.c_double, P]),
             "kfo_pressure": (C.c_double, [I, P, C.c_double]),
             "kfo_sound_speed": (C.c_double, [I, P, C.c_double]),
@@ -149,6 +150,17 @@ class Oracle:
         assert U_local.shape[0] == np_planes + 2 * H
         self._chk(self.L.kfo_slab_rhs(C.byref(self.cfg), self.rset.c_table, int(p0),
                                       int(np_planes), _p(U_local), _p(out), self.nthreads), "slab_rhs")
+        return out
+
+    def fill_ghost(self, U):
+        """The domain padded with R+1 ghost cells per side (fill_ghost,
+        S:553-561), shape (n_z+2H,) n_y+2H, n_x+2H, nvar."""
+        g = self.grid
+        H = g.radius + 1
+        shape = tuple(n + 2 * H for n in g.shape) + (g.nvar,)
+        out = np.zeros(shape)
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        self._chk(lib().kfo_fill_ghost(C.byref(self.cfg), _p(U), _p(out)), "fill_ghost")
         return out
 
     def max_speed(self, U):

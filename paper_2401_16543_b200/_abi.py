@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KFVM_LIB") or os.path.join(_HERE, "libkfvm_b200.so")
 
 KFVM_OK, KFVM_ERR_CONFIG, KFVM_ERR_RUNTIME, KFVM_ERR_DEVICE = 0, 1, 2, 3
-BC_PERIODIC, BC_OUTFLOW = 0, 1
+BC_PERIODIC, BC_OUTFLOW, BC_REFLECTING, BC_DIRICHLET, BC_SLIT = 0, 1, 2, 3, 4
 RIEMANN_HLLC, RIEMANN_HLL = 0, 1
 IC_FOURIER, IC_VORONOI, IC_FOURIER_SPHERE, IC_UNIFORM, IC_VORTEX, IC_DENSITY_WAVE = range(6)
 
@@ -45,6 +45,9 @@ class KfvmConfig(C.Structure):
         ("safety", C.c_double), ("dt_min", C.c_double), ("dt_max", C.c_double),
         ("viscous", C.c_int), ("reynolds", C.c_double), ("prandtl", C.c_double),
         ("mach", C.c_double), ("inv_froude2", C.c_double),
+        ("bc_per_side", C.c_int), ("bc_side", C.c_int * 6),
+        ("bc_state", (C.c_double * 5) * 6), ("slit_center", (C.c_double * 2) * 6),
+        ("slit_radius", C.c_double * 6),
     ]
 
 

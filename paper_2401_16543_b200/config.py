@@ -17,6 +17,11 @@ import numpy as np
 from . import _abi
 
 
+_BC_KINDS = {"periodic": _abi.BC_PERIODIC, "outflow": _abi.BC_OUTFLOW,
+             "reflecting": _abi.BC_REFLECTING, "dirichlet": _abi.BC_DIRICHLET,
+             "slit": _abi.BC_SLIT}
+
+
 @dataclass(frozen=True)
 class GridConfig:
     dim: int = 2
@@ -24,7 +29,13 @@ class GridConfig:
     nx: int = 64
     ny: int = 64
     nz: int = 1
-    bc: str = "periodic"        # "periodic" | "outflow"
+    bc: str = "periodic"        # "periodic" | "outflow" | "reflecting": every side
+    # per-side kinds (BoundaryKind S:534-537), order x-lo, x-hi, y-lo, y-hi
+    # [, z-lo, z-hi]; each "periodic" | "outflow" | "reflecting" | "dirichlet"
+    # | "slit".  None = `bc` on every side.
+    sides: tuple | None = None
+    side_states: tuple | None = None  # per side: conservative state (dirichlet, slit inflow) or None
+    slits: tuple | None = None        # per side: (centre (tangential axes), radius) or None
     riemann: str = "hllc"       # "hllc" | "hll"   (riemann.solver)
     dx: float | None = None     # defaults to 1/nx (unit domain)
     gamma: float = 1.4
@@ -52,8 +63,21 @@ class GridConfig:
             raise ValueError("dim must be 2 or 3")
         if self.radius not in (2, 3):
             raise ValueError("unsupported stencil radius (must be 2 or 3)")
-        if self.bc not in ("periodic", "outflow"):
-            raise ValueError("bc must be periodic or outflow")
+        if self.bc not in ("periodic", "outflow", "reflecting"):
+            raise ValueError("bc must be periodic, outflow or reflecting")
+        if self.sides is not None:
+            ns = 2 * self.dim
+            if len(self.sides) != ns or any(k not in _BC_KINDS for k in self.sides):
+                raise ValueError(f"sides needs {ns} kinds from {sorted(_BC_KINDS)}")
+            for a in range(self.dim):
+                if (self.sides[2 * a] == "periodic") != (self.sides[2 * a + 1] == "periodic"):
+                    raise ValueError("periodic sides come in matching pairs (S:536)")
+            for q, k in enumerate(self.sides):
+                st = self.side_states[q] if self.side_states else None
+                if k in ("dirichlet", "slit") and (st is None or len(st) != self.nvar):
+                    raise ValueError(f"side {q} ({k}) needs a {self.nvar}-component state")
+                if k == "slit" and not (self.slits and self.slits[q] and self.slits[q][1] > 0):
+                    raise ValueError(f"side {q} needs a slit (centre, radius > 0)")
         if self.integrator not in ("ssprk3", "ssp43"):
             raise ValueError("integrator must be ssprk3 or ssp43")
         if self.riemann not in ("hllc", "hll"):
@@ -85,7 +109,20 @@ class GridConfig:
         c = _abi.KfvmConfig()
         c.dim, c.radius = self.dim, self.radius
         c.nx, c.ny, c.nz = self.nx, self.ny, (self.nz if self.dim == 3 else 1)
-        c.bc = _abi.BC_PERIODIC if self.bc == "periodic" else _abi.BC_OUTFLOW
+        c.bc = _BC_KINDS[self.bc]
+        if self.sides is not None:
+            c.bc_per_side = 1
+            for q, k in enumerate(self.sides):
+                c.bc_side[q] = _BC_KINDS[k]
+                st = self.side_states[q] if self.side_states else None
+                if st is not None:
+                    for v, x in enumerate(st):
+                        c.bc_state[q][v] = float(x)
+                sl = self.slits[q] if self.slits else None
+                if sl is not None:
+                    for m, x in enumerate(sl[0]):
+                        c.slit_center[q][m] = float(x)
+                    c.slit_radius[q] = float(sl[1])
         c.riemann = _abi.RIEMANN_HLLC if self.riemann == "hllc" else _abi.RIEMANN_HLL
         c.dx = float(self.dx if self.dx is not None else 1.0 / self.nx)
         c.gamma, c.cfl, c.eps = self.gamma, self.cfl, self.eps

@@ -61,8 +61,8 @@ struct Chunk {
   int e0, e1;             // extended planes whose states a states launch computes
 };
 
-__device__ __forceinline__ int remap(int i, int n, int bc) {
-  if (bc == KFVM_BC_PERIODIC) {
+__device__ __forceinline__ int remap(int i, int n, int periodic) {
+  if (periodic) {
     // stencil offsets are at most R+1 cells beyond an edge: one conditional
     // wrap covers every grid with n >= R+1; the modulo is the rare fallback
     i = i < 0 ? i + n : (i >= n ? i - n : i);
@@ -73,6 +73,47 @@ __device__ __forceinline__ int remap(int i, int n, int bc) {
     return i;
   }
   return i < 0 ? 0 : (i >= n ? n - 1 : i);
+}
+
+// Ghost-cell index map of one axis for the side's boundary kind (fill_ghost,
+// S:553-561): periodic wrap, reflecting mirror image, otherwise the nearest
+// interior cell (outflow; dirichlet/slit cells that take the fixed state
+// ignore the source).
+__device__ __forceinline__ int bc_src(int i, int n, int kind) {
+  if (i >= 0 && i < n) return i;
+  if (kind == KFVM_BC_PERIODIC) return remap(i, n, 1);
+  if (kind == KFVM_BC_REFLECTING) return i < 0 ? -1 - i : 2 * n - 1 - i;
+  return i < 0 ? 0 : n - 1;
+}
+
+// Value transform of one crossed side (physical axis a, side s) for variable
+// v of the ghost cell at physical coordinates c: reflecting negates the
+// wall-normal momentum, dirichlet writes the fixed state, a slit writes the
+// inflow state strictly inside r^2 < radius^2.
+__device__ __forceinline__ double bc_value(double u, int a, int s, int v, const int* c) {
+  const int side = 2 * a + s, kind = c_k.bcs[side];
+  if (kind == KFVM_BC_REFLECTING) return v == 1 + a ? -u : u;
+  if (kind == KFVM_BC_DIRICHLET) return c_k.bst[side][v];
+  if (kind == KFVM_BC_SLIT) {
+    double r2 = 0.0;
+    int m = 0;
+    for (int t = 0; t < c_k.dim; ++t) {
+      if (t == a) continue;
+      const double d = ((double)c[t] + 0.5) * c_k.dx - c_k.slc[side][m];
+      r2 = m == 0 ? d * d : r2 + d * d;
+      ++m;
+    }
+    if (r2 < c_k.slr2[side]) return c_k.bst[side][v];
+  }
+  return u;
+}
+
+// value of variable v at ghost cell c (physical coordinates, extents n) from
+// its source value u: the per-axis transforms composed in axis order x, y, z
+__device__ __forceinline__ double bc_compose(double u, int v, const int* c, const int* n) {
+  for (int a = 0; a < c_k.dim; ++a)
+    if (c[a] < 0 || c[a] >= n[a]) u = bc_value(u, a, c[a] >= n[a], v, c);
+  return u;
 }
 
 // padded-storage offsets of x, mid row j, local plane p (ghosts included)
@@ -372,9 +413,10 @@ __global__ void k_dt(unsigned long long* smax, double* dt_cur, double* dt_seq, i
   *smax = 0ULL;
 }
 
-// slab-axis halo planes from the rank's own planes (1 rank: wrap/clamp; end
-// ranks with outflow: clamp).  which: bit0 = low side, bit1 = high side.
-__global__ void k_halo_local(double* __restrict__ U, Geo g, int nv, int nglob, int which) {
+// slab-axis halo planes of a global end from the rank's own planes (whole
+// padded planes, so the corner ghosts compose as T_slab(T_mid(T_x(U)))).
+// which: bit0 = low side, bit1 = high side.
+__global__ void k_halo_local(double* __restrict__ U, Geo g, int nv, int nglob, int p0, int which) {
   const long long per = (long long)g.H * g.pstride;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= 2 * per * nv) return;
@@ -385,28 +427,31 @@ __global__ void k_halo_local(double* __restrict__ U, Geo g, int nv, int nglob, i
   const long long e = r % per;
   const int l = (int)(e / g.pstride);
   const long long o = e % g.pstride;
-  int p, src;
-  if (side == 0) {
-    p = -g.H + l;
-  } else {
-    p = g.np_loc + l;
-  }
-  if (g.np_loc == nglob)
-    src = remap(p, nglob, c_k.bc);
-  else
-    src = p < 0 ? 0 : g.np_loc - 1;  // outflow clamp at a global end
-  U[v * g.vstride + (long long)(p + g.H) * g.pstride + o] =
-      U[v * g.vstride + (long long)(src + g.H) * g.pstride + o];
+  const int p = side == 0 ? -g.H + l : g.np_loc + l;
+  const int sa = c_k.dim - 1;
+  const int src = bc_src(p0 + p, nglob, c_k.bcs[2 * sa + side]) - p0;
+  int c[3], n[3];
+  c[0] = (int)(o % g.nxp) - g.xo;
+  n[0] = g.nx;
+  c[1] = (int)(o / g.nxp) - g.Gm;  // 3-D mid row (2-D: overwritten below)
+  n[1] = g.nm;
+  c[sa] = p0 + p;
+  n[sa] = nglob;
+  const double u = U[v * g.vstride + (long long)(src + g.H) * g.pstride + o];
+  U[v * g.vstride + (long long)(p + g.H) * g.pstride + o] = bc_value(u, sa, side, v, c);
 }
 
 // Ghost cells (fill_ghost) in one launch: every ghost cell of the
 // padded local block — the x ghost columns and mid ghost rows of the planes
 // [-hp, np + hp) and, with hp = H (one rank), the interior block of the
 // slab-axis halo planes — gets the value of the cell its boundary kinds map
-// to, the maps composed over the axes (periodic wrap / outflow clamp).  With
+// to, the index maps and value transforms composed over the axes in order
+// x, mid, slab (bc_src / bc_compose: periodic wrap, outflow clamp,
+// reflecting mirror with the normal momentum negated, dirichlet / slit
+// inflow states).  With
 // several ranks (hp = 0) the halo planes are exchanged afterwards as whole
 // padded planes.
-__global__ void k_ghost(double* __restrict__ U, Geo g, int nv, int nsa, int hp) {
+__global__ void k_ghost(double* __restrict__ U, Geo g, int nv, int nsa, int p0, int hp) {
   const int P = g.np_loc + 2 * hp, rows = g.nm + 2 * g.Gm;
   const long long nA = 2LL * g.G * rows * P, nB = 2LL * g.Gm * g.nx * P,
                   nC = 2LL * hp * g.nm * g.nx, n = nA + nB + nC;
@@ -435,12 +480,23 @@ __global__ void k_ghost(double* __restrict__ U, Geo g, int nv, int nsa, int hp) 
     const int l = (int)(e / g.nm);
     p = l < hp ? l - hp : g.np_loc + l - hp;
   }
-  const int xs = remap(x, g.nx, c_k.bc);
-  const int js = g.Gm ? remap(j, g.nm, c_k.bc) : j;
-  const int ps = hp ? remap(p, nsa, c_k.bc) : p;
+  // physical coordinates and extents (the slab axis is y in 2-D, z in 3-D)
+  const int sa = c_k.dim - 1;
+  int c[3], ext[3];
+  c[0] = x;
+  ext[0] = g.nx;
+  if (sa == 2) {
+    c[1] = j;
+    ext[1] = g.nm;
+  }
+  c[sa] = p0 + p;
+  ext[sa] = nsa;
+  const int xs = bc_src(x, g.nx, c_k.bcs[x < 0 ? 0 : 1]);
+  const int js = g.Gm ? bc_src(j, g.nm, c_k.bcs[j < 0 ? 2 : 3]) : j;
+  const int ps = hp ? bc_src(p, nsa, c_k.bcs[2 * sa + (p < 0 ? 0 : 1)]) : p;
   const long long vb = v * g.vstride;
-  U[vb + (long long)(p + g.H) * g.pstride + moff(g, j) + xoff(g, x)] =
-      U[vb + (long long)(ps + g.H) * g.pstride + moff(g, js) + xoff(g, xs)];
+  const double u = U[vb + (long long)(ps + g.H) * g.pstride + moff(g, js) + xoff(g, xs)];
+  U[vb + (long long)(p + g.H) * g.pstride + moff(g, j) + xoff(g, x)] = bc_compose(u, v, c, ext);
 }
 
 // AoS (host order) <-> SoA interior planes
@@ -853,7 +909,7 @@ void ghost(kfvm_handle* h, double* U) {
   const long long n = 2LL * g.G * (g.nm + 2 * g.Gm) * P + 2LL * g.Gm * g.nx * P +
                       2LL * hp * g.nm * g.nx;
   tic(h);
-  k_ghost<<<blocks(n * h->nv, 256), 256, 0, h->stream>>>(U, g, h->nv, h->nsa, hp);
+  k_ghost<<<blocks(n * h->nv, 256), 256, 0, h->stream>>>(U, g, h->nv, h->nsa, h->p0, hp);
   h->launches++;
   toc(h, &h->t_other);
 }
@@ -866,14 +922,14 @@ int halo(kfvm_handle* h, double* U, cudaStream_t st) {
     (void)per;  // k_ghost filled the halo planes
   } else {
     NcclApi& N = nccl();
-    const bool periodic = h->cfg.bc == KFVM_BC_PERIODIC;
+    const bool periodic = h->kc.per[h->dim - 1] != 0;
     const int lo = h->rank - 1, hi = h->rank + 1;
     const bool has_lo = periodic || lo >= 0, has_hi = periodic || hi < h->nranks;
     const int plo = (lo + h->nranks) % h->nranks, phi = hi % h->nranks;
     int which = (has_lo ? 0 : 1) | (has_hi ? 0 : 2);
     if (which) {
       k_halo_local<<<blocks(2 * per * h->nv, 256), 256, 0, st>>>(U, h->g, h->nv, h->nsa,
-                                                                         which);
+                                                                         h->p0, which);
       h->launches++;
     }
     // per peer pair the order is: upward transfer (my top interior -> the
@@ -966,7 +1022,7 @@ int kx_flags(kfvm_handle* h, const double* U, const Chunk& ch) {
   h->launches += 3;
   if (h->nranks > 1) {
     NcclApi& N = nccl();
-    const bool periodic = h->cfg.bc == KFVM_BC_PERIODIC;
+    const bool periodic = h->kc.per[h->dim - 1] != 0;
     const int lo = h->rank - 1, hi = h->rank + 1;
     const bool has_lo = periodic || lo >= 0, has_hi = periodic || hi < h->nranks;
     const int plo = (lo + h->nranks) % h->nranks, phi = hi % h->nranks;
@@ -1359,6 +1415,51 @@ extern "C" int kfvm_nccl_unique_id(unsigned char id[128]) {
   return KFVM_OK;
 }
 
+// Boundary kinds per physical side (bc, or bc_side[] when bc_per_side) into
+// the device constants; false for an invalid combination: unknown kind,
+// unpaired periodic side, a mirror deeper than the axis (reflecting needs
+// n >= R+1), an inadmissible dirichlet / inflow state, a non-positive slit.
+static bool resolve_bcs(const kfvm_config* cfg, DevConsts* k) {
+  const int dim = cfg->dim, H = cfg->radius + 1;
+  const int n[3] = {cfg->nx, cfg->ny, dim == 3 ? cfg->nz : 1};
+  const double gm1 = cfg->gamma - 1.0;
+  for (int a = 0; a < 3; ++a) {
+    for (int s = 0; s < 2; ++s) {
+      const int side = 2 * a + s;
+      int kind = cfg->bc_per_side ? cfg->bc_side[side] : cfg->bc;
+      if (a >= dim) kind = KFVM_BC_PERIODIC;
+      if (kind < KFVM_BC_PERIODIC || kind > KFVM_BC_SLIT) return false;
+      if (!cfg->bc_per_side && kind > KFVM_BC_REFLECTING) return false;
+      if (kind == KFVM_BC_REFLECTING && n[a] < H) return false;
+      k->bcs[side] = kind;
+      for (int v = 0; v < 5; ++v) k->bst[side][v] = 0.0;
+      k->slc[side][0] = k->slc[side][1] = 0.0;
+      k->slr2[side] = 0.0;
+      if (kind == KFVM_BC_DIRICHLET || kind == KFVM_BC_SLIT) {
+        const double* u = cfg->bc_state[side];
+        for (int v = 0; v < dim + 2; ++v) {
+          if (!std::isfinite(u[v])) return false;
+          k->bst[side][v] = u[v];
+        }
+        double q = 0.0;
+        for (int m = 0; m < dim; ++m) q += u[1 + m] * u[1 + m];
+        if (!(u[0] > 0.0) || !(gm1 * (u[dim + 1] - 0.5 * q / u[0]) > 0.0)) return false;
+      }
+      if (kind == KFVM_BC_SLIT) {
+        const double r = cfg->slit_radius[side];
+        if (!(r > 0.0) || !std::isfinite(r)) return false;
+        k->slc[side][0] = cfg->slit_center[side][0];
+        k->slc[side][1] = cfg->slit_center[side][1];
+        k->slr2[side] = r * r;
+      }
+    }
+    const bool p0 = k->bcs[2 * a] == KFVM_BC_PERIODIC, p1 = k->bcs[2 * a + 1] == KFVM_BC_PERIODIC;
+    if (p0 != p1) return false;  // periodic sides come in matching pairs
+    k->per[a] = p0 ? 1 : 0;
+  }
+  return true;
+}
+
 extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, const kfvm_dist* dist,
                                kfvm_handle** out) {
   if (!cfg || !t || !out) return KFVM_ERR_CONFIG;
@@ -1367,12 +1468,15 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
       t->dim != cfg->dim || t->radius != cfg->radius)
     return KFVM_ERR_CONFIG;
   if (cfg->nx < 1 || cfg->ny < 1 || (cfg->dim == 3 && cfg->nz < 1) || !(cfg->dx > 0) ||
-      (cfg->bc != KFVM_BC_PERIODIC && cfg->bc != KFVM_BC_OUTFLOW) ||
       (cfg->riemann != KFVM_RIEMANN_HLLC && cfg->riemann != KFVM_RIEMANN_HLL))
     return KFVM_ERR_CONFIG;
   if (cfg->viscous && !(cfg->reynolds > 0 && cfg->prandtl > 0 && cfg->mach > 0))
     return KFVM_ERR_CONFIG;  // the viscous terms need Re, Pr, Ma
   if (!std::isfinite(cfg->inv_froude2)) return KFVM_ERR_CONFIG;
+  {
+    DevConsts probe{};
+    if (!resolve_bcs(cfg, &probe)) return KFVM_ERR_CONFIG;
+  }
   kfvm_handle* h = new kfvm_handle();
   h->cfg = *cfg;
   h->dim = cfg->dim;
@@ -1422,6 +1526,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   k.R = cfg->radius;
   k.riemann = cfg->riemann;
   k.bc = cfg->bc;
+  resolve_bcs(cfg, &k);
   k.n[0] = cfg->nx;
   k.n[1] = h->g.nm;
   k.n[2] = h->nsa;

@@ -137,7 +137,6 @@ __global__ void __launch_bounds__(256) k_kx_flag(const double* __restrict__ U,
                              : __longlong_as_double(0x7ff8000000000000LL);
   bool nan = !(Q == Q);
   double jmax = 0.0;
-  const bool periodic = c_k.bc == KFVM_BC_PERIODIC;
   const int pg = p0g + p, pc = c - 1;  // chunk-relative interior plane
 #pragma unroll
   for (int d = 0; d < D; ++d) {
@@ -145,7 +144,8 @@ __global__ void __launch_bounds__(256) k_kx_flag(const double* __restrict__ U,
     for (int side = 0; side < 2; ++side) {
       const int coord = d == 0 ? x : (d == D - 1 ? pg : j);
       const int n = d == 0 ? g.nx : (d == D - 1 ? nsa : g.nm);
-      if (!periodic && ((side == 0 && coord == 0) || (side == 1 && coord == n - 1))) continue;
+      // physical-boundary faces of non-periodic axes are exempt
+      if (!c_k.per[d] && ((side == 0 && coord == 0) || (side == 1 && coord == n - 1))) continue;
       const int fa = x + (d == 0 ? side : 0);
       const int fb = j + ((D == 3 && d == 1) ? side : 0);
       const int fc = pc + (d == D - 1 ? side : 0);
@@ -158,7 +158,9 @@ __global__ void __launch_bounds__(256) k_kx_flag(const double* __restrict__ U,
 }
 
 // Flags of the extended box's ghost cells: the flag of the cell they
-// replicate (periodic image / outflow clamp).  Slab-axis neighbours owned by
+// replicate (periodic image; the nearest interior cell for every other kind
+// — with one ghost layer the reflecting mirror image is that cell, and the
+// dirichlet / slit ghosts take the flag of the cell they border).  Slab-axis neighbours owned by
 // another rank were received into extended planes 0 and C+1 (x, mid interior
 // positions) before this runs.
 template <int D>
@@ -173,14 +175,15 @@ __global__ void __launch_bounds__(256) k_kx_mirror(unsigned char* __restrict__ f
   const bool xin = x >= 0 && x < g.nx, jin = D == 2 || (j >= 0 && j < g.nm);
   const bool pin = c >= 1 && c <= ch.C;
   if (xin && jin && pin) return;
-  const int xt = remap(x, g.nx, c_k.bc), jt = D == 3 ? remap(j, g.nm, c_k.bc) : 0;
+  // one ghost layer: the reflecting mirror image is the clamp
+  const int xt = remap(x, g.nx, c_k.per[0]), jt = D == 3 ? remap(j, g.nm, c_k.per[1]) : 0;
   int ct = c;
   if (!pin) {
     const int pg = p0g + ch.c0 - 1 + c;  // global plane of this extended plane
     const bool outside = pg < 0 || pg >= nsa;
-    if (nranks == 1 || (outside && c_k.bc != KFVM_BC_PERIODIC)) {
+    if (nranks == 1 || (outside && !c_k.per[D - 1])) {
       // replicated plane is local: periodic wrap (one rank) or outflow clamp
-      const int pt = remap(pg, nsa, c_k.bc) - p0g;  // local plane index
+      const int pt = remap(pg, nsa, c_k.per[D - 1]) - p0g;  // local plane index
       ct = pt - (ch.c0 - 1);
     } else if (xin && jin) {
       return;  // received from the neighbouring rank

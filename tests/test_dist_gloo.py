@@ -53,11 +53,30 @@ def halo_exchange(U_loc, H, np_loc, rank, ws, bc):
     U_loc[np_loc + H:] = recv_hi if has_hi else U_loc[np_loc + H - 1:np_loc + H]
 
 
-def worker(rank, ws, port, idx, n, steps, q):
+def _walls_grid(g):
+    """Per-side boundary kinds with wall / inflow kinds at the slab ends
+    (the library rebuilds the planes beyond a non-periodic global end)."""
+    from dataclasses import replace
+    gam = g.gamma
+    if g.dim == 2:
+        st = (1.2, 0.4, 0.0, 1.0 / (gam - 1) + 0.5 * 1.2 * 0.16 / 1.44)
+        return replace(g, sides=("dirichlet", "outflow", "reflecting", "dirichlet"),
+                       side_states=(st, None, None, st))
+    jet = (1.4, 0.0, 0.0, 1.4, 1.0 / (gam - 1) + 0.5 * 1.4)
+    return replace(g, sides=("reflecting", "outflow", "periodic", "periodic", "reflecting", "slit"),
+                   side_states=(None, None, None, None, None, jet),
+                   slits=(None, None, None, None, None, ((0.5, 0.5), 0.3)))
+
+
+def _grid(idx, n, walls):
+    w = K.baseline_config(idx, n=n)
+    return w, (_walls_grid(w.grid) if walls else w.grid)
+
+
+def worker(rank, ws, port, idx, n, steps, q, walls=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=ws)
-    w = K.baseline_config(idx, n=n)
-    g = w.grid
+    w, g = _grid(idx, n, walls)
     rset = K.precompute(g.radius, dim=g.dim)
     o = Oracle(g, rset, nthreads=2)
     import ctypes as C
@@ -76,7 +95,8 @@ def worker(rank, ws, port, idx, n, steps, q):
         for stage in (1, 2, 3):
             loc = np.zeros((np_loc + 2 * H,) + U.shape[1:])
             loc[H:H + np_loc] = Uk
-            halo_exchange(loc, H, np_loc, rank, ws, g.bc)
+            slab_bc = g.sides[2 * (g.dim - 1)] if g.sides else g.bc
+            halo_exchange(loc, H, np_loc, rank, ws, slab_bc)
             L = o.slab_rhs(loc, p0, np_loc)
             Uk = o.combine(stage, U0, Uk, L, dt)
         U = Uk
@@ -88,12 +108,14 @@ def worker(rank, ws, port, idx, n, steps, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("idx,n,steps", [(1, 20, 2), (2, 16, 2), (3, 10, 1), (4, 10, 1)])
-def test_gloo_two_ranks_bitwise(idx, n, steps):
+@pytest.mark.parametrize("idx,n,steps,walls", [(1, 20, 2, False), (2, 16, 2, False),
+                                               (3, 10, 1, False), (4, 10, 1, False),
+                                               (1, 20, 2, True), (3, 10, 1, True)])
+def test_gloo_two_ranks_bitwise(idx, n, steps, walls):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, idx, n, steps, q)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, 2, port, idx, n, steps, q, walls)) for r in range(2)]
     for p in procs:
         p.start()
     parts, dts = q.get(timeout=300)
@@ -101,8 +123,8 @@ def test_gloo_two_ranks_bitwise(idx, n, steps):
         p.join(timeout=60)
         assert p.exitcode == 0
     Ud = np.concatenate([u for _, u in parts], axis=0)
-    w = K.baseline_config(idx, n=n)
-    U0 = K.initial_condition(w.grid, w.ic)
-    U1, d1 = Oracle(w.grid, K.precompute(w.grid.radius, dim=w.grid.dim)).run(U0, steps)
+    w, g = _grid(idx, n, walls)
+    U0 = K.initial_condition(g, w.ic)
+    U1, d1 = Oracle(g, K.precompute(g.radius, dim=g.dim)).run(U0, steps)
     assert np.array_equal(np.array(dts), d1)
     assert np.array_equal(Ud, U1)
