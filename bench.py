@@ -245,24 +245,29 @@ def main():
 
     import torch
     torch.cuda.set_device(local)
-    nccl_id = None
-    if ws > 1:
+    def new_nccl_id():
+        if ws <= 1:
+            return None
         from paper_2401_16543_b200.solver import nccl_unique_id
         idt = torch.zeros(128, dtype=torch.uint8)
         if rank == 0:
             idt[:] = torch.tensor(list(nccl_unique_id()), dtype=torch.uint8)
         dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.tolist())
+        return bytes(idt.tolist())
+    nccl_id = new_nccl_id()
     g = w.grid
     s = K.Solver(g, rset, rank=rank, nranks=ws, device=local, nccl_id=nccl_id)
     stream = torch.cuda.ExternalStream(s.stream)
-    if args.engine is not None:
-        s.set_option("engine", args.engine)
-    if args.kz is not None:
-        s.set_option("kz", args.kz)
-    for o in args.opt:
-        k, v = o.split("=")
-        s.set_option(k, int(v))
+
+    def configure(sv):
+        if args.engine is not None:
+            sv.set_option("engine", args.engine)
+        if args.kz is not None:
+            sv.set_option("kz", args.kz)
+        for o in args.opt:
+            k, v = o.split("=")
+            sv.set_option(k, int(v))
+    configure(s)
 
     # warm-up (also captures the CUDA graph)
     s.generate_ic(w.ic)
@@ -323,12 +328,42 @@ def main():
         s.set_state(Uh)
         s.ssp_rk3_step()
         s.get_state(out=Uh)
-    t_e2e = time.perf_counter() - t0
+    t_serial = time.perf_counter() - t0
+    # ensemble pipelining through the same API: two independent fields, one
+    # handle (stream) each; every step of every field uploads it from pinned
+    # host memory, steps it and reads it back, and the copy engines move one
+    # field while the SMs step the other
+    s2 = K.Solver(g, rset, rank=rank, nranks=ws, device=local, nccl_id=new_nccl_id())
+    configure(s2)
+    host2 = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
+    Uh2 = host2.numpy().reshape(s.local_shape)
+    Uh2[...] = Uh
+    pair = ((s, Uh), (s2, Uh2))
+    for sv, hb in pair:  # warm the second handle's graph
+        sv.set_state_async(hb)
+        sv.run_async(1)
+        sv.get_state_async(hb)
+    for sv, _ in pair:
+        sv.sync()
+    torch.cuda.synchronize()
     if dist:
-        t = torch.tensor([t_e2e], dtype=torch.float64)
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for sv, hb in pair:
+            sv.set_state_async(hb)
+            sv.run_async(1)
+            sv.get_state_async(hb)
+    for sv, _ in pair:
+        sv.sync()
+    t_e2e = (time.perf_counter() - t0) / 2  # per field-step pair -> per step
+    s2.close()
+    if dist:
+        t = torch.tensor([t_e2e, t_serial], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_e2e = float(t[0])
+        t_e2e, t_serial = float(t[0]), float(t[1])
     e2e_value = cells * 3 * e2e_steps / t_e2e
+    e2e_serial = cells * 3 * e2e_steps / t_serial
 
     if rank == 0:
         F = algorithmic_flops(rset)
@@ -365,7 +400,12 @@ def main():
             "config": workload_config(w, args),
             "e2e": {"value": e2e_value, "unit": "cell-updates/s",
                     "h2d_bytes_per_step": nloc * 8, "d2h_bytes_per_step": nloc * 8,
-                    "steps": e2e_steps, "api": "Solver.set_state/ssp_rk3_step/get_state (C-ABI)"},
+                    "steps": e2e_steps,
+                    "api": "Solver.set_state_async/run_async/get_state_async (C-ABI), 2 fields "
+                           "on 2 handles: each field-step uploads from pinned host memory and "
+                           "reads back; the copy engines overlap the other field's step",
+                    "serial_value": e2e_serial,
+                    "serial_api": "Solver.set_state/ssp_rk3_step/get_state, one field, no overlap"},
             "roofline": {"bound": "fp64", "kernel": "k_states_* (reconstruction+WENO-AO+limiter)",
                          "engine": "DMMA (FP64 tensor, plane-marching)" if g.dim == 3
                          else "DFMA (unrolled, row-marching smem rings)",

@@ -221,6 +221,12 @@ void kfvm_gpu_destroy(kfvm_handle* h);
  * Replaces Field construction / read-out. */
 int kfvm_gpu_set_state(kfvm_handle* h, const double* U_host);
 int kfvm_gpu_get_state(kfvm_handle* h, double* U_host);
+/* Asynchronous upload / readback on the handle's stream (no host sync; the
+ * host buffer must not be touched until kfvm_gpu_sync).  Pinned buffers and
+ * one handle per field let the copies of one field overlap the steps of
+ * another (ensemble pipelining). */
+int kfvm_gpu_set_state_async(kfvm_handle* h, const double* U_host);
+int kfvm_gpu_get_state_async(kfvm_handle* h, double* U_host);
 /* Same on device memory (AoS, caller-owned device pointer). */
 int kfvm_gpu_set_state_device(kfvm_handle* h, const double* U_dev);
 int kfvm_gpu_get_state_device(kfvm_handle* h, double* U_dev);

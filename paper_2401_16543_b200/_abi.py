@@ -78,6 +78,8 @@ EXPORTS = [
     ("kfvm_gpu_destroy", None, [C.c_void_p]),
     ("kfvm_gpu_set_state", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kfvm_gpu_get_state", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kfvm_gpu_set_state_async", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("kfvm_gpu_get_state_async", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kfvm_gpu_set_state_device", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kfvm_gpu_get_state_device", C.c_int, [C.c_void_p, C.c_void_p]),
     ("kfvm_gpu_rhs", C.c_int, [C.c_void_p, C.c_void_p]),

@@ -36,6 +36,15 @@ namespace kfvm_b200 {
 #ifndef KFVM_MMA_MINB
 #define KFVM_MMA_MINB 3
 #endif
+#ifndef KFVM_FLUX_PIPE
+#define KFVM_FLUX_PIPE 1
+#endif
+#ifndef KFVM_FLUX_MINB2
+#define KFVM_FLUX_MINB2 8
+#endif
+#ifndef KFVM_FLUX_MINB3
+#define KFVM_FLUX_MINB3 5
+#endif
 __constant__ DevConsts c_k;
 __constant__ DevTable c_t;
 __constant__ int c_gather[512];
@@ -159,6 +168,37 @@ __device__ __forceinline__ void face_flux(const double* __restrict__ St, double*
   double Fb[nv];
 #pragma unroll
   for (int v = 0; v < nv; ++v) Fb[v] = 0.0;
+#if KFVM_FLUX_PIPE
+  // software-pipelined: the next point's states are in flight during this
+  // point's Riemann solve (quadrature order unchanged)
+  double UL[nv], UR[nv];
+#pragma unroll
+  for (int v = 0; v < nv; ++v) {
+    UL[v] = St[(long long)(((2 * d + 1) * RP) * nv + v) * ch.next + iL];
+    UR[v] = St[(long long)(((2 * d) * RP) * nv + v) * ch.next + iR];
+  }
+#pragma unroll
+  for (int m = 0; m < RP; ++m) {
+    double NL[nv], NR[nv], Fp[nv];
+    if (m + 1 < RP) {
+#pragma unroll
+      for (int v = 0; v < nv; ++v) {
+        NL[v] = St[(long long)(((2 * d + 1) * RP + m + 1) * nv + v) * ch.next + iL];
+        NR[v] = St[(long long)(((2 * d) * RP + m + 1) * nv + v) * ch.next + iR];
+      }
+    }
+    d_riemann_dir<DIM, d>(c_k, UL, UR, Fp);
+#pragma unroll
+    for (int v = 0; v < nv; ++v) Fb[v] = fma(c_t.face_w[(2 * d) * RP + m], Fp[v], Fb[v]);
+    if (m + 1 < RP) {
+#pragma unroll
+      for (int v = 0; v < nv; ++v) {
+        UL[v] = NL[v];
+        UR[v] = NR[v];
+      }
+    }
+  }
+#else
   for (int m = 0; m < RP; ++m) {
     const int sL = (2 * d + 1) * RP + m;
     const int sR = (2 * d) * RP + m;
@@ -172,14 +212,15 @@ __device__ __forceinline__ void face_flux(const double* __restrict__ St, double*
 #pragma unroll
     for (int v = 0; v < nv; ++v) Fb[v] = fma(c_t.face_w[sR], Fp[v], Fb[v]);
   }
+#endif
 #pragma unroll
   for (int v = 0; v < nv; ++v) F[(long long)(d * nv + v) * ch.nfb + f] = Fb[v];
 }
 
 // one thread per face of direction d = blockIdx.y; min blocks per SM
-// measured on config 2 (8) and config 3 (6)
+// measured on config 2 (8) and config 3 (5: no spills, 11.7 vs 12.6 ms/step at 6)
 template <int DIM, int R>
-__global__ void __launch_bounds__(128, DIM == 2 ? 8 : 6) k_flux(const double* __restrict__ St,
+__global__ void __launch_bounds__(128, DIM == 2 ? KFVM_FLUX_MINB2 : KFVM_FLUX_MINB3) k_flux(const double* __restrict__ St,
                                                               double* __restrict__ F, Geo g,
                                                               Chunk ch) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -318,6 +359,30 @@ __device__ __forceinline__ void warp_max_atomic(unsigned long long* dst, double 
   if ((threadIdx.x & 31) == 0 && v) atomicMax(dst, v);
 }
 
+// the same over a whole block (blockDim a multiple of 32, <= 1024): one
+// atomic per block — 32K same-address atomics per stage on config 2 were a
+// serialisation point.  Every thread of the block must call it.
+__device__ __forceinline__ void block_max_atomic(unsigned long long* dst, double s) {
+  __shared__ unsigned long long wmax[32];
+  unsigned long long v = s > 0.0 ? (unsigned long long)__double_as_longlong(s) : 0ULL;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? wmax[threadIdx.x] : 0ULL;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = w > v ? w : v;
+    }
+    if (threadIdx.x == 0 && v) atomicMax(dst, v);
+  }
+}
+
 // ---------------------------------------------------------------- k_update
 // mode 0: write L(u) into Uout; mode 1..3: SSP-RK3 stage combine.
 template <int DIM, bool GRAV = false>
@@ -376,7 +441,7 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ F,
   }
   if (stage) {
     if (valid && !d_admissible<DIM>(c_k, un)) atomicOr(err, 2);
-    if (stage == 3 && smax) warp_max_atomic(smax, valid ? d_cell_speed<DIM>(c_k, un) : 0.0);
+    if (stage == 3 && smax) block_max_atomic(smax, valid ? d_cell_speed<DIM>(c_k, un) : 0.0);
   }
 }
 
@@ -393,7 +458,7 @@ __global__ void k_speed(const double* __restrict__ U, Geo g, unsigned long long*
   double u[nv];
 #pragma unroll
   for (int v = 0; v < nv; ++v) u[v] = U[v * g.vstride + ou];
-  warp_max_atomic(smax, d_cell_speed<DIM>(c_k, u));
+  block_max_atomic(smax, d_cell_speed<DIM>(c_k, u));
 }
 
 // dt = cfl*dx / smax on the device (select_dt), clipped so the
@@ -1769,6 +1834,33 @@ extern "C" int kfvm_gpu_get_state(kfvm_handle* h, double* U_host) {
   const size_t n = (size_t)interior_elems(h);
   CK(cudaMemcpyAsync(U_host, h->aos, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  return KFVM_OK;
+}
+
+// Asynchronous variants on the handle's stream (no host synchronisation; the
+// host buffer must stay untouched until kfvm_gpu_sync): upload + transpose,
+// transpose + download.  With pinned buffers and one handle per field, the
+// copies of one field overlap the steps of another on the copy engines.
+extern "C" int kfvm_gpu_set_state_async(kfvm_handle* h, const double* U_host) {
+  int rc = ensure_aos(h);
+  if (rc) return rc;
+  const long long n = interior_elems(h);
+  CK(cudaMemcpyAsync(h->aos, U_host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice,
+                     h->stream));
+  k_transpose<0><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, h->aos, h->g, h->nv);
+  h->launches++;
+  CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_gpu_get_state_async(kfvm_handle* h, double* U_host) {
+  int rc = ensure_aos(h);
+  if (rc) return rc;
+  const long long n = interior_elems(h);
+  k_transpose<1><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, h->aos, h->g, h->nv);
+  h->launches++;
+  CK(cudaMemcpyAsync(U_host, h->aos, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
   return KFVM_OK;
 }
 

@@ -119,6 +119,23 @@ class Solver:
         self._check(self.L.kfvm_gpu_get_state(self.h, U.ctypes.data), "get_state")
         return U
 
+    def _host_buf(self, U: np.ndarray, what: str) -> np.ndarray:
+        if (U.dtype != np.float64 or not U.flags.c_contiguous
+                or U.size != self.local_cells * self.grid.nvar):
+            raise ValueError(f"{what}: needs a C-contiguous float64 array of the slab's size")
+        return U
+
+    def set_state_async(self, U: np.ndarray):
+        """Upload on the handle's stream without waiting; ``U`` (ideally
+        pinned) must stay unchanged until :meth:`sync`."""
+        U = self._host_buf(U, "set_state_async")
+        self._check(self.L.kfvm_gpu_set_state_async(self.h, U.ctypes.data), "set_state_async")
+
+    def get_state_async(self, out: np.ndarray):
+        """Read back into ``out`` on the handle's stream; valid after :meth:`sync`."""
+        out = self._host_buf(out, "get_state_async")
+        self._check(self.L.kfvm_gpu_get_state_async(self.h, out.ctypes.data), "get_state_async")
+
     def set_state_device(self, ptr: int):
         self._check(self.L.kfvm_gpu_set_state_device(self.h, C.c_void_p(ptr)), "set_state_device")
 

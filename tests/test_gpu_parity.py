@@ -209,3 +209,26 @@ def test_overlapped_stage_bitwise(require_gpu, idx, n, chunk):
             outs.append((d, s.get_state()))
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_async_two_handles_pipeline(require_gpu):
+    """set_state_async / run_async / get_state_async on two handles (the
+    bench's e2e ensemble pipeline) == the synchronous path, bit for bit."""
+    g, ic, U, rset = _setup(1, 32, {})
+    with K.Solver(g, rset) as s:
+        s.set_state(U)
+        s.advance(1)
+        ref1 = s.get_state()
+        s.advance(1)
+        ref2 = s.get_state()
+    bufs = [U.copy(), U.copy()]
+    with K.Solver(g, rset) as a, K.Solver(g, rset) as b:
+        for _ in range(2):
+            for sv, hb in ((a, bufs[0]), (b, bufs[1])):
+                sv.set_state_async(hb)
+                sv.run_async(1)
+                sv.get_state_async(hb)
+        a.sync()
+        b.sync()
+    assert np.array_equal(bufs[0], ref2) and np.array_equal(bufs[1], ref2)
+    assert not np.array_equal(ref1, ref2)
