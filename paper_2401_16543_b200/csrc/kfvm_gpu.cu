@@ -416,26 +416,37 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ F,
   const long long ou = uidx<DIM>(g, a, b, ch.c0 + c);
   const double dt = stage ? *dtp : 0.0;
   double un[nv];
+  // every load of the cell issued before any arithmetic (memory-level
+  // parallelism; the operation order below is unchanged)
+  double fr[DIM][nv][2], u0v[nv], ukv[nv];
 #pragma unroll
   for (int v = 0; v < nv; ++v) {
-    double acc = F[(long long)(0 * nv + v) * ch.nfb + fh[0]] - F[(long long)(0 * nv + v) * ch.nfb + f0];
-    acc = acc + (F[(long long)(1 * nv + v) * ch.nfb + fh[1]] - F[(long long)(1 * nv + v) * ch.nfb + f0]);
-    if (DIM == 3)
-      acc = acc + (F[(long long)(2 * nv + v) * ch.nfb + fh[2]] - F[(long long)(2 * nv + v) * ch.nfb + f0]);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      fr[d][v][0] = F[(long long)(d * nv + v) * ch.nfb + fh[d]];
+      fr[d][v][1] = F[(long long)(d * nv + v) * ch.nfb + f0];
+    }
+    ukv[v] = Uk[v * g.vstride + ou];
+    u0v[v] = stage > 1 ? U0[v * g.vstride + ou] : ukv[v];
+  }
+#pragma unroll
+  for (int v = 0; v < nv; ++v) {
+    double acc = fr[0][v][0] - fr[0][v][1];
+    acc = acc + (fr[1][v][0] - fr[1][v][1]);
+    if (DIM == 3) acc = acc + (fr[DIM - 1][v][0] - fr[DIM - 1][v][1]);
     double L = -(acc / c_k.dx);
     if (GRAV) {  // gravity source from the cell average (P eq rtSource)
-      if (v == 2) L = L + c_k.g2 * Uk[ou];
-      if (v == nv - 1) L = L + c_k.g2 * Uk[2 * g.vstride + ou];
+      if (v == 2) L = L + c_k.g2 * ukv[0];
+      if (v == nv - 1) L = L + c_k.g2 * ukv[2];
     }
     if (stage == 0) {
       un[v] = L;
     } else if (stage > 10) {
       double uh = 0.0;
-      un[v] = d_combine43(stage, U0[v * g.vstride + ou], Uk[v * g.vstride + ou], L, dt, &uh);
+      un[v] = d_combine43(stage, U0[v * g.vstride + ou], ukv[v], L, dt, &uh);
       if (stage == 13 && valid) Uhat[v * g.vstride + ou] = uh;
     } else {
-      un[v] = d_combine(stage, U0[v * g.vstride + ou], Uk[v * g.vstride + ou], L, dt, c_k.c13,
-                        c_k.c23);
+      un[v] = d_combine(stage, u0v[v], ukv[v], L, dt, c_k.c13, c_k.c23);
     }
     if (valid) Uout[v * g.vstride + ou] = un[v];
   }
