@@ -39,6 +39,9 @@ namespace kfvm_b200 {
 #ifndef KFVM_FLUX_PIPE
 #define KFVM_FLUX_PIPE 1
 #endif
+#ifndef KFVM_UPD_MINB
+#define KFVM_UPD_MINB 1
+#endif
 #ifndef KFVM_FLUX_MINB2
 #define KFVM_FLUX_MINB2 8
 #endif
@@ -386,7 +389,7 @@ __device__ __forceinline__ void block_max_atomic(unsigned long long* dst, double
 // ---------------------------------------------------------------- k_update
 // mode 0: write L(u) into Uout; mode 1..3: SSP-RK3 stage combine.
 template <int DIM, bool GRAV = false>
-__global__ void __launch_bounds__(256) k_update(const double* __restrict__ F,
+__global__ void __launch_bounds__(256, KFVM_UPD_MINB) k_update(const double* __restrict__ F,
                                                 const double* __restrict__ U0,
                                                 const double* __restrict__ Uk,
                                                 double* __restrict__ Uout, Geo g, Chunk ch,
