@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--n", type=int, default=None, help="override resolution (testing)")
+    ap.add_argument("--nz", type=int, default=None,
+                    help="slab-axis extent (e.g. config 5's weak-scaling block 1024x1024x128)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", type=int, default=None,
@@ -228,7 +230,7 @@ def main():
     args = ap.parse_args()
 
     import paper_2401_16543_b200 as K
-    w = K.baseline_config(args.config, n=args.n)
+    w = K.baseline_config(args.config, n=args.n, nz=args.nz)
     if args.kxrcf:
         from dataclasses import replace as _replace
         w = _replace(w, grid=_replace(w.grid, kxrcf=True))

@@ -1703,17 +1703,27 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     bad(cudaMemset(h->Ua, 0, ufull * sizeof(double)), "memset");
     bad(cudaMemset(h->Ub, 0, ufull * sizeof(double)), "memset");
   }
-  // chunk planes so the face-state scratch stays within budget
+  // chunk planes so the face-state and flux scratch stay within budget: half
+  // the device memory still free after the state buffers (at least
+  // st_budget = 16 GB when that much is free), so large 3-D slabs run in few
+  // chunks (each chunk recomputes its two edge planes)
   {
-    const long long per_plane = (long long)(h->g.nx + 2) * (h->dim == 3 ? h->g.nm + 2 : 1) *
-                                h->NP * h->nv * (long long)sizeof(double);
-    long long c = h->st_budget / per_plane - 2;
+    const long long per_plane =
+        ((long long)(h->g.nx + 2) * (h->dim == 3 ? h->g.nm + 2 : 1) * h->NP +
+         (long long)(h->g.nx + 1) * (h->dim == 3 ? h->g.nm + 1 : 1) * h->dim) *
+        h->nv * (long long)sizeof(double);
+    size_t fr = 0, tot = 0;
+    if (rc == KFVM_OK) cudaMemGetInfo(&fr, &tot);
+    long long budget = (long long)(0.5 * (double)fr);
+    if (budget < h->st_budget) budget = std::min(h->st_budget, (long long)(0.8 * (double)fr));
+    long long c = budget / per_plane - 2;
     c = std::max(1LL, std::min(c, (long long)np));
     h->chunk = (int)c;
     if (h->kx && h->chunk < np) {
       // the flags of a chunk's edge planes need the pass-1 states beyond them
       rc = KFVM_ERR_CONFIG;
-      h->err = "kxrcf: the slab's face states must fit one chunk (16 GB scratch)";
+      h->err = "kxrcf: the slab's face states must fit one chunk (scratch budget: half the "
+               "free device memory)";
     }
   }
   if (h->kx && rc == KFVM_OK) {
