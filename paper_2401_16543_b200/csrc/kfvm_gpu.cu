@@ -717,6 +717,7 @@ struct kfvm_handle {
   double *St = nullptr, *F = nullptr, *aos = nullptr;
   size_t st_elems = 0, f_elems = 0, aos_elems = 0;
   int chunk = 0;
+  int ring_split = 1;  // option "ring_split": ring columns by k_states_fast
   int *d_gather = nullptr;
   double *d_face = nullptr, *d_deriv = nullptr;
   double *d_dt_seq = nullptr, *d_dt_cur = nullptr;
@@ -874,13 +875,30 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
       return;
     }
   }
+  // ring split: when the two ring columns of the extended box would cost a
+  // mostly-empty last 32-cell segment (e.g. 258 = 8 x 32 + 2 at 256^3), the
+  // segment engines cover the interior x range and the unrolled DFMA engine
+  // computes the ring columns (same bits: every engine runs the pinned
+  // contract)
+  const int xsp = (Gen<DIM, R>::UNROLLED && h->ring_split &&
+                   (ch.ex - 2 + 31) / 32 < (ch.ex + 31) / 32) ? 1 : 0;
+  auto ring = [&]() {
+    if (!xsp) return;
+    const long long nr = 2LL * ch.em * (ch.e1 - ch.e0);
+    if constexpr (Gen<DIM, R>::UNROLLED)
+      k_states_fast<DIM, R, true><<<(unsigned)((nr + 31) / 32), 32 * (DIM + 2), 0, h->stream>>>(
+          U, h->Pr, h->St, h->g, ch, h->d_err);
+    h->launches++;
+  };
   if constexpr (DIM == 2) {
     if (h->engine == 4) {
       const int KZ = h->kz;
-      const long long nblk4 = (long long)((ch.ex + 31) / 32) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
+      const long long nblk4 =
+          (long long)((ch.ex - 2 * xsp + 31) / 32) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
       k_stage_row<R, false><<<(unsigned)nblk4, 128, 0, h->stream>>>(U, h->Pr, h->St, h->F, h->g,
-                                                                    ch, KZ, h->d_err);
+                                                                    ch, KZ, h->d_err, nullptr, xsp);
       h->launches++;
+      ring();
       toc(h, &h->t_states);
       return;
     }
@@ -888,9 +906,10 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   if (h->engine == 2) {
     const int KZ = h->kz;
     const long long nblk2 =
-        (long long)((ch.ex + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
+        (long long)((ch.ex - 2 * xsp + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
     k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
-        U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4);
+        U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, nullptr, xsp);
+    ring();
     dbg_sync(h, "k_states_u");
     if (UCfg<DIM, R>::NG > 1) {
       h->launches++;
@@ -2150,6 +2169,11 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
       h->engine = value ? 2 : 0;
     }
     drop_graphs(h);
+    return KFVM_OK;
+  }
+  if (n == "ring_split") {
+    drop_graphs(h);
+    h->ring_split = value ? 1 : 0;
     return KFVM_OK;
   }
   if (n == "overlap") {

@@ -51,7 +51,8 @@ template <int R, bool FUSE, bool KX = false, bool P1 = false>
 __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
     k_stage_row(const double* __restrict__ U, const double* __restrict__ Pr,
                 double* __restrict__ St, double* __restrict__ F, Geo g, Chunk ch, int KZ,
-                int* __restrict__ err, const unsigned char* __restrict__ kfl = nullptr) {
+                int* __restrict__ err, const unsigned char* __restrict__ kfl = nullptr,
+                int xsp = 0) {
   constexpr int D = 2, nv = 4;
   using G = Gen<2, R>;
   using C = RowCfg<R>;
@@ -68,13 +69,15 @@ __global__ void __launch_bounds__(128, KFVM_ROW_MINB(R))
   double* sSt = sW;
 
   const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
-  const int nseg = (ch.ex + 31) >> 5;
+  // xsp = 1 (FUSE = false): the segments cover the interior x range only (the
+  // two ring columns are computed by k_states_fast<2, R, true>)
+  const int nseg = (ch.ex - 2 * xsp + 31) >> 5;
   const int seg = blockIdx.x % nseg;
   const int zblk = blockIdx.x / nseg;
   const int cstart = ch.e0 + zblk * KZ, cend = min(ch.e1, cstart + KZ);
-  const int x0 = seg * 32 - 1;  // x of the segment's first extended cell
-  const int a = seg * 32 + lane;
-  const bool active = a < ch.ex;
+  const int x0 = xsp + seg * 32 - 1;  // x of the segment's first extended cell
+  const int a = xsp + seg * 32 + lane;
+  const bool active = a < ch.ex - xsp;
   const int xr = lane + R;   // the lane's cell in a ring row
   const int icn = lane + 1;  // the lane's cell in a prims row
 

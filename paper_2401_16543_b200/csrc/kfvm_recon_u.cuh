@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     k_states_u(const double* __restrict__ U, const double* __restrict__ Pr,
                double* __restrict__ St, Geo g, Chunk ch, int KZ, int* __restrict__ err,
                const double* __restrict__ Bd, const double* __restrict__ Bf,
-               const int* __restrict__ gat4, const unsigned char* __restrict__ kfl = nullptr) {
+               const int* __restrict__ gat4, const unsigned char* __restrict__ kfl = nullptr,
+               int xsp = 0) {
   using G = Gen<D, R>;
   using C = UCfg<D, R>;
   constexpr int nv = C::nv, NP = G::NP, NS = G::NS, ND = C::ND, NPT = C::NPT;
@@ -113,7 +114,9 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
   const double* Bdp = C::BSMEM ? sBd : Bd;
   const double* Bfp = C::BSMEM ? sBf : Bf;
 
-  const int nseg = (ch.ex + 31) >> 5;
+  // xsp = 1: the segments cover the interior x range only (the two ring
+  // columns of the extended box are computed by k_states_fast<.., true>)
+  const int nseg = (ch.ex - 2 * xsp + 31) >> 5;
   int bid = blockIdx.x;
   const int seg = bid % nseg;
   bid /= nseg;
@@ -121,19 +124,19 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
   const int zblk = bid / ch.em;
   const int cstart = ch.e0 + zblk * KZ, cend = min(ch.e1, cstart + KZ);
   const int j = D == 3 ? b - 1 : 0;
-  const int x0 = seg * 32 - 1;        // x of the segment's first cell
+  const int x0 = xsp + seg * 32 - 1;  // x of the segment's first cell
   // warp w owns the cells w, w+4, ..., w+28 of the segment (stride 4): the 4
   // slots of a DMMA chunk are mostly consecutive x offsets, and with stride-4
   // rows the 16 (cell, slot) words of a half-warp fall in distinct banks
   const int cidx = w + 4 * r8;
-  const int a = seg * 32 + cidx;  // extended x index of this lane's cell
-  const bool active = a < ch.ex;
+  const int a = xsp + seg * 32 + cidx;  // extended x index of this lane's cell
+  const bool active = a < ch.ex - xsp;
   const int xr = cidx + R;            // the cell's x in the region
   if constexpr (KXM) {  // KXRCF: a tile without a flagged cell has nothing to do
     bool any = false;
     for (int i = threadIdx.x; i < 32 * (cend - cstart); i += 128) {
-      const int ai = seg * 32 + (i & 31), ci = cstart + (i >> 5);
-      any |= ai < ch.ex && kfl[((long long)ci * ch.em + b) * ch.ex + ai];
+      const int ai = xsp + seg * 32 + (i & 31), ci = cstart + (i >> 5);
+      any |= ai < ch.ex - xsp && kfl[((long long)ci * ch.em + b) * ch.ex + ai];
     }
     if (!__syncthreads_or(any)) return;
   }

@@ -334,3 +334,24 @@ def test_gpu_walls_chunked_and_overlapped(require_gpu, dim, opts):
         dts = s.advance(2)
         assert np.array_equal(dts, dto)
         assert np.array_equal(s.get_state(), Uo)
+
+
+@pytest.mark.gpu
+def test_gpu_walls_ring_split(require_gpu):
+    """nx = 32 (ring split: ring columns by the DFMA engine) with reflecting /
+    dirichlet x sides, 3-D tensor engine, both settings of the split."""
+    st = tuple(P.cons(GAM, 1.2, (0.4, 0.0, 0.0), 1.0))
+    g = GridConfig(dim=3, radius=2, nx=32, ny=6, nz=6, cfl=0.4,
+                   sides=("dirichlet", "reflecting", "periodic", "periodic", "outflow", "outflow"),
+                   side_states=(st, None, None, None, None, None))
+    rng = np.random.default_rng(23)
+    U = P.cons(GAM, 1.0 + 0.2 * rng.random(g.shape), [0.2 * (rng.random(g.shape) - 0.5) for _ in range(3)],
+               1.0 + 0.2 * rng.random(g.shape))
+    rset = K.precompute(2, dim=3)
+    Uo, dto = Oracle(g, rset).run(U, 2)
+    for split in (0, 1):
+        with K.Solver(g, rset) as s:
+            s.set_option("ring_split", split)
+            s.set_state(U)
+            assert np.array_equal(s.advance(2), dto)
+            assert np.array_equal(s.get_state(), Uo)

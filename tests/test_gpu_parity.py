@@ -33,6 +33,10 @@ CASES = [
     ("cfg3_3d_r2_periodic_fourier", 3, 16, 2, {}),
     ("cfg4_3d_r2_outflow_voronoi", 4, 14, 2, {}),
     ("cfg5_3d_r3_periodic_sphere", 5, 12, 1, {}),
+    # nx = 32 / 64: the segment engines cover interior x, the ring columns
+    # come from k_states_fast (ring split)
+    ("cfg3_3d_r2_ring_split", 3, 32, 1, {}),
+    ("cfg2_2d_r2_ring_split", 2, 64, 2, {}),
 ]
 
 
