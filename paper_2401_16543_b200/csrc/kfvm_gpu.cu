@@ -39,8 +39,11 @@ namespace kfvm_b200 {
 #ifndef KFVM_FLUX_PIPE
 #define KFVM_FLUX_PIPE 1
 #endif
-#ifndef KFVM_UPD_MINB
-#define KFVM_UPD_MINB 1
+// k_update CTAs per SM (2-D): 3 measured 0.130 vs 0.161 ms/step at 1 (config 2;
+// 4: 0.128 with spills);
+// 3-D keeps 1 (2.15 vs 2.97 ms/step at 4, config 3)
+#ifndef KFVM_UPD_MINB2
+#define KFVM_UPD_MINB2 3
 #endif
 #ifndef KFVM_FLUX_MINB2
 #define KFVM_FLUX_MINB2 8
@@ -389,7 +392,7 @@ __device__ __forceinline__ void block_max_atomic(unsigned long long* dst, double
 // ---------------------------------------------------------------- k_update
 // mode 0: write L(u) into Uout; mode 1..3: SSP-RK3 stage combine.
 template <int DIM, bool GRAV = false>
-__global__ void __launch_bounds__(256, KFVM_UPD_MINB) k_update(const double* __restrict__ F,
+__global__ void __launch_bounds__(256, DIM == 2 ? KFVM_UPD_MINB2 : 1) k_update(const double* __restrict__ F,
                                                 const double* __restrict__ U0,
                                                 const double* __restrict__ Uk,
                                                 double* __restrict__ Uout, Geo g, Chunk ch,
@@ -880,7 +883,9 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   // segment engines cover the interior x range and the unrolled DFMA engine
   // computes the ring columns (same bits: every engine runs the pinned
   // contract)
-  const int xsp = (Gen<DIM, R>::UNROLLED && h->ring_split &&
+  // (3-D only: in 2-D the ring columns are ~2k cells, a 65-CTA launch whose
+  // latency (13 us) exceeds the saved segment (10 us), measured config 2)
+  const int xsp = (DIM == 3 && Gen<DIM, R>::UNROLLED && h->ring_split &&
                    (ch.ex - 2 + 31) / 32 < (ch.ex + 31) / 32) ? 1 : 0;
   auto ring = [&]() {
     if (!xsp) return;

@@ -33,10 +33,9 @@ CASES = [
     ("cfg3_3d_r2_periodic_fourier", 3, 16, 2, {}),
     ("cfg4_3d_r2_outflow_voronoi", 4, 14, 2, {}),
     ("cfg5_3d_r3_periodic_sphere", 5, 12, 1, {}),
-    # nx = 32 / 64: the segment engines cover interior x, the ring columns
-    # come from k_states_fast (ring split)
+    # nx = 32: the segment engine covers interior x, the ring columns come
+    # from k_states_fast (3-D ring split)
     ("cfg3_3d_r2_ring_split", 3, 32, 1, {}),
-    ("cfg2_2d_r2_ring_split", 2, 64, 2, {}),
 ]
 
 

@@ -6,12 +6,8 @@ python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log
 for c in 1 3; do python bench.py --config $c --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_c$c.log 2>&1; tail -1 gpurun_out/bench_c$c.log | cut -c1-150; done
 python bench.py --config 4 --n 256 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_c4_256.log 2>&1
 python bench.py --config 5 --n 256 --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_c5_256.log 2>&1
+python bench.py --config 4 --steps 10 --warmup 3 --no-cpu > gpurun_out/bench_c4_full.log 2>&1
+python bench.py --config 5 --n 1024 --nz 128 --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_c5_block.log 2>&1
 for c in 2 3; do python bench.py --config $c --steps 5 --warmup 3 --no-cpu --kxrcf > gpurun_out/bench_c${c}_kx.log 2>&1; done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_l.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py --config 3 --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_l3.log 2>&1
-rm -f gpurun_out/prof_c2_states.ncu-rep gpurun_out/prof_c2_flux.ncu-rep gpurun_out/prof_c2_update.ncu-rep gpurun_out/prof_c3_states_128.ncu-rep
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stage_row -s 3 -c 1 -o gpurun_out/prof_c2_states python tools/profile_step.py --config 2 --steps 2 > gpurun_out/ncu1.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_flux -s 3 -c 1 -o gpurun_out/prof_c2_flux python tools/profile_step.py --config 2 --steps 2 > gpurun_out/ncu2.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_update -s 3 -c 1 -o gpurun_out/prof_c2_update python tools/profile_step.py --config 2 --steps 2 > gpurun_out/ncu4.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_states_u -s 3 -c 1 -o gpurun_out/prof_c3_states_128 python tools/profile_step.py --config 3 --n 128 --steps 2 > gpurun_out/ncu3.log 2>&1
-ls gpurun_out/*.ncu-rep
