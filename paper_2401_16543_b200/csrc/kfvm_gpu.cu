@@ -36,9 +36,6 @@ namespace kfvm_b200 {
 #ifndef KFVM_MMA_MINB
 #define KFVM_MMA_MINB 3
 #endif
-#ifndef KFVM_FLUX_PIPE
-#define KFVM_FLUX_PIPE 1
-#endif
 // k_update CTAs per SM (2-D): 3 measured 0.130 vs 0.161 ms/step at 1 (config 2;
 // 4: 0.128 with spills);
 // 3-D keeps 1 (2.15 vs 2.97 ms/step at 4, config 3)
@@ -174,7 +171,6 @@ __device__ __forceinline__ void face_flux(const double* __restrict__ St, double*
   double Fb[nv];
 #pragma unroll
   for (int v = 0; v < nv; ++v) Fb[v] = 0.0;
-#if KFVM_FLUX_PIPE
   // software-pipelined: the next point's states are in flight during this
   // point's Riemann solve (quadrature order unchanged)
   double UL[nv], UR[nv];
@@ -204,21 +200,6 @@ __device__ __forceinline__ void face_flux(const double* __restrict__ St, double*
       }
     }
   }
-#else
-  for (int m = 0; m < RP; ++m) {
-    const int sL = (2 * d + 1) * RP + m;
-    const int sR = (2 * d) * RP + m;
-    double UL[nv], UR[nv], Fp[nv];
-#pragma unroll
-    for (int v = 0; v < nv; ++v) {
-      UL[v] = St[(long long)(sL * nv + v) * ch.next + iL];
-      UR[v] = St[(long long)(sR * nv + v) * ch.next + iR];
-    }
-    d_riemann_dir<DIM, d>(c_k, UL, UR, Fp);
-#pragma unroll
-    for (int v = 0; v < nv; ++v) Fb[v] = fma(c_t.face_w[sR], Fp[v], Fb[v]);
-  }
-#endif
 #pragma unroll
   for (int v = 0; v < nv; ++v) F[(long long)(d * nv + v) * ch.nfb + f] = Fb[v];
 }
@@ -352,22 +333,10 @@ __global__ void __launch_bounds__(128) k_visc(const double* __restrict__ Pr, dou
 
 #include "kfvm_kxrcf.cuh"
 
-// max of non-negative doubles through their bit patterns (exact, order-free):
-// one atomic per warp instead of one per cell.  Must be called by all lanes
-// that reached it: callers never exit early (whole warps stay converged).
-__device__ __forceinline__ void warp_max_atomic(unsigned long long* dst, double s) {
-  unsigned long long v = s > 0.0 ? (unsigned long long)__double_as_longlong(s) : 0ULL;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = w > v ? w : v;
-  }
-  if ((threadIdx.x & 31) == 0 && v) atomicMax(dst, v);
-}
-
-// the same over a whole block (blockDim a multiple of 32, <= 1024): one
-// atomic per block — 32K same-address atomics per stage on config 2 were a
-// serialisation point.  Every thread of the block must call it.
+// max of non-negative doubles through their bit patterns (exact, order-free)
+// over a whole block (blockDim a multiple of 32, <= 1024): one
+// atomic per block instead of one per warp.  Every thread of the block must
+// call it.
 __device__ __forceinline__ void block_max_atomic(unsigned long long* dst, double s) {
   __shared__ unsigned long long wmax[32];
   unsigned long long v = s > 0.0 ? (unsigned long long)__double_as_longlong(s) : 0ULL;
