@@ -355,3 +355,31 @@ def test_gpu_walls_ring_split(require_gpu):
             s.set_state(U)
             assert np.array_equal(s.advance(2), dto)
             assert np.array_equal(s.get_state(), Uo)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("R", [2, 3])
+def test_gpu_3d_kxrcf_walls(require_gpu, R):
+    """KXRCF mode (pass-1 states, flags with wall faces exempt, WENO on
+    flagged cells) with reflecting / dirichlet / outflow sides in 3-D."""
+    n = 12
+    st = tuple(P.cons(GAM, 2.0, (0.5, 0.0, 0.0), 3.0))
+    g = GridConfig(dim=3, radius=R, nx=n, ny=n, nz=n, cfl=0.3, kxrcf=True,
+                   sides=("dirichlet", "outflow", "reflecting", "reflecting", "reflecting", "outflow"),
+                   side_states=(st, None, None, None, None, None))
+    rng = np.random.default_rng(29)
+    # a density / pressure jump so that some cells are flagged
+    x = (np.arange(n) + 0.5) / n
+    jump = np.broadcast_to(x > 0.5, g.shape)
+    rho = np.where(jump, 0.5, 1.5) + 1e-4 * rng.random(g.shape)
+    p = np.where(jump, 0.4, 1.2)
+    U = P.cons(GAM, rho, [1e-4 * (rng.random(g.shape) - 0.5) for _ in range(3)], p)
+    rset = K.precompute(R, dim=3)
+    o = Oracle(g, rset)
+    Uo, dto = o.run(U, 2)
+    with K.Solver(g, rset) as s:
+        fl = s.kxrcf_flags(U)
+        assert np.array_equal(fl, o.kxrcf_flags(U)) and 0 < fl.sum() < fl.size
+        s.set_state(U)
+        assert np.array_equal(s.advance(2), dto)
+        assert np.array_equal(s.get_state(), Uo)
