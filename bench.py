@@ -183,12 +183,15 @@ def run_reference(args, w, rset, rank):
     print(json.dumps(line), flush=True)
 
 
-def traffic_of(config_index):
+def traffic_of(config_index, shape):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/r01/roofline_traffic.json), or None."""
+    capture of this exact workload (profiles/r01/roofline_traffic.json), or
+    None."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
             t = json.load(f)[str(config_index)]
+        if list(t["shape"]) != list(shape):
+            return None, None
         return (t["dram_read_bytes"] + t["dram_write_bytes"],
                 "dram read+write bytes per launch, ncu --set full: profiles/r01/" + t["capture"])
     except Exception:
@@ -427,8 +430,8 @@ def main():
                          "frac": (achieved / fp64) if achieved and not g.kxrcf else None,
                          "peak_source": fp64_src,
                          "algorithmic_flops_per_cell_stage": None if g.kxrcf else F,
-                         "traffic": None if g.kxrcf else traffic_of(w.index)[0],
-                         "traffic_source": None if g.kxrcf else traffic_of(w.index)[1]},
+                         "traffic": None if g.kxrcf else traffic_of(w.index, g.shape)[0],
+                         "traffic_source": None if g.kxrcf else traffic_of(w.index, g.shape)[1]},
             "kernel_ms_per_step": kt,
             "kxrcf": ({"enabled": True, "flagged_fraction_final_state": kx_frac}
                       if g.kxrcf else {"enabled": False}),
