@@ -683,6 +683,10 @@ struct kfvm_handle {
   std::vector<int> gather;
   int dim = 0, R = 0, nv = 0, NP = 0;
   int nsa = 0, p0 = 0, rank = 0, nranks = 1, device = 0;
+  // the NCCL slab path is on: several ranks, or KFVM_FORCE_NCCL=1 on one rank
+  // (a one-rank communicator with self send/recv: exercises the multi-GPU
+  // code path on a single GPU)
+  bool multi = false;
   Geo g{};
   double *U0 = nullptr, *Ua = nullptr, *Ub = nullptr;
   double* Pr = nullptr;  // k_prims output: p, c, 1/rho, u_d per cell (incl. halos)
@@ -977,7 +981,7 @@ void update(kfvm_handle* h, const Chunk& ch, const double* U0, const double* Uk,
 // ghost cells of the local block (one rank: the halo planes too)
 void ghost(kfvm_handle* h, double* U) {
   const Geo& g = h->g;
-  const int hp = h->nranks == 1 ? g.H : 0, P = g.np_loc + 2 * hp;
+  const int hp = !h->multi ? g.H : 0, P = g.np_loc + 2 * hp;
   const long long n = 2LL * g.G * (g.nm + 2 * g.Gm) * P + 2LL * g.Gm * g.nx * P +
                       2LL * hp * g.nm * g.nx;
   tic(h);
@@ -990,7 +994,7 @@ void ghost(kfvm_handle* h, double* U) {
 int halo(kfvm_handle* h, double* U, cudaStream_t st) {
   const long long per = (long long)h->g.H * h->g.pstride;
   tic(h);
-  if (h->nranks == 1) {
+  if (!h->multi) {
     (void)per;  // k_ghost filled the halo planes
   } else {
     NcclApi& N = nccl();
@@ -1026,7 +1030,7 @@ int halo(kfvm_handle* h, double* U, cudaStream_t st) {
 }
 
 int reduce_smax(kfvm_handle* h) {
-  if (h->nranks == 1) return KFVM_OK;
+  if (!h->multi) return KFVM_OK;
   // positive doubles order like their bit patterns: max on uint64 is exact
   if (nccl().AllReduce(h->d_smax, h->d_smax, 1, kNcclUint64, kNcclMax, h->comm, h->stream) != 0)
     return fail(h, KFVM_ERR_DEVICE, "ncclAllReduce failed");
@@ -1092,7 +1096,7 @@ int kx_flags(kfvm_handle* h, const double* U, const Chunk& ch) {
   k_kx_flag<DIM><<<blocks(ch.next, 256), 256, 0, h->stream>>>(U, h->Pr, h->F, h->d_flags, h->g,
                                                               ch, h->p0, h->nsa);
   h->launches += 3;
-  if (h->nranks > 1) {
+  if (h->multi) {
     NcclApi& N = nccl();
     const bool periodic = h->kc.per[h->dim - 1] != 0;
     const int lo = h->rank - 1, hi = h->rank + 1;
@@ -1108,7 +1112,7 @@ int kx_flags(kfvm_handle* h, const double* U, const Chunk& ch) {
     if (N.GroupEnd() != 0) return fail(h, KFVM_ERR_DEVICE, "ncclGroupEnd failed (flags)");
   }
   k_kx_mirror<DIM><<<blocks(ch.next, 256), 256, 0, h->stream>>>(h->d_flags, h->g, ch, h->p0,
-                                                                h->nsa, h->nranks);
+                                                                h->nsa, h->multi ? 1 : 0);
   h->launches++;
   toc(h, &h->t_other);
   return KFVM_OK;
@@ -1340,10 +1344,10 @@ int enqueue_attempt43(kfvm_handle* h) {
   else
     k_err_rows<3><<<blocks(nr, 128), 128, 0, h->stream>>>(h->Ub, h->Uh, h->d_rows, h->g);
   double* loc = h->d_planes + (long long)h->nranks * h->npmax;  // this rank's partials
-  k_err_planes<<<blocks(np, 128), 128, 0, h->stream>>>(h->d_rows, h->nranks > 1 ? loc : h->d_planes,
+  k_err_planes<<<blocks(np, 128), 128, 0, h->stream>>>(h->d_rows, h->multi ? loc : h->d_planes,
                                                        nrow, np);
   h->launches += 2;
-  if (h->nranks > 1) {
+  if (h->multi) {
     if (nccl().AllGather(loc, h->d_planes, (size_t)h->npmax, kNcclDouble, h->comm, h->stream) != 0)
       return fail(h, KFVM_ERR_DEVICE, "ncclAllGather failed (error norm)");
   }
@@ -1575,6 +1579,10 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   }
   int np;
   kfvm_slab_range(h->nsa, h->nranks, h->rank, &h->p0, &np);
+  {
+    const char* fe = std::getenv("KFVM_FORCE_NCCL");
+    h->multi = h->nranks > 1 || (fe && fe[0] == '1');
+  }
   h->g.nx = cfg->nx;
   h->g.nm = cfg->dim == 3 ? cfg->ny : 1;
   h->g.np_loc = np;
@@ -1770,19 +1778,22 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   bad(cudaStreamCreateWithFlags(&h->s_halo, cudaStreamNonBlocking), "stream");
   bad(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming), "event");
   bad(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming), "event");
-  h->overlap = h->nranks > 1 ? 1 : 0;
+  h->overlap = h->multi ? 1 : 0;
   bad(cudaEventCreate(&h->ev[0]), "event");
   bad(cudaEventCreate(&h->ev[1]), "event");
   if (rc == KFVM_OK) rc = ensure_dt_cap(h, 1024);
-  if (rc == KFVM_OK && h->nranks > 1) {
+  if (rc == KFVM_OK && h->multi) {
     NcclApi& N = nccl();
     if (!N.ok) {
       rc = KFVM_ERR_DEVICE;
       h->err = "libnccl.so.2 not loadable";
     } else {
       nccl_uid u;
-      std::memcpy(u.internal, dist->nccl_id, 128);
-      if (N.CommInitRank(&h->comm, h->nranks, u, h->rank) != 0) {
+      if (dist && h->nranks > 1)
+        std::memcpy(u.internal, dist->nccl_id, 128);
+      else if (N.GetUniqueId(&u) != 0)  // KFVM_FORCE_NCCL: a one-rank communicator
+        rc = KFVM_ERR_DEVICE;
+      if (rc == KFVM_OK && N.CommInitRank(&h->comm, h->nranks, u, h->rank) != 0) {
         rc = KFVM_ERR_DEVICE;
         h->err = "ncclCommInitRank failed";
       }
@@ -1985,7 +1996,7 @@ extern "C" int kfvm_gpu_run_async(kfvm_handle* h, int nsteps) {
   if (rc) return rc;
   CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
   if ((rc = enqueue_speed(h))) return rc;
-  if (h->timing || h->nranks > 1) {
+  if (h->timing || h->multi) {
     for (int s = 0; s < nsteps; ++s)
       if ((rc = enqueue_step(h))) return rc;
     return KFVM_OK;

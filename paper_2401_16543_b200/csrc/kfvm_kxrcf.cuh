@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_kx_flag(const double* __restrict__ U,
 // positions) before this runs.
 template <int D>
 __global__ void __launch_bounds__(256) k_kx_mirror(unsigned char* __restrict__ fl, Geo g,
-                                                   Chunk ch, int p0g, int nsa, int nranks) {
+                                                   Chunk ch, int p0g, int nsa, int exchanged) {
   const long long tid = (long long)blockIdx.x * 256 + threadIdx.x;
   if (tid >= ch.next) return;
   const int a = (int)(tid % ch.ex);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256) k_kx_mirror(unsigned char* __restrict__ f
   if (!pin) {
     const int pg = p0g + ch.c0 - 1 + c;  // global plane of this extended plane
     const bool outside = pg < 0 || pg >= nsa;
-    if (nranks == 1 || (outside && !c_k.per[D - 1])) {
+    if (!exchanged || (outside && !c_k.per[D - 1])) {
       // replicated plane is local: periodic wrap (one rank) or outflow clamp
       const int pt = remap(pg, nsa, c_k.per[D - 1]) - p0g;  // local plane index
       ct = pt - (ch.c0 - 1);
