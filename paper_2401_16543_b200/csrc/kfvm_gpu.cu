@@ -1561,7 +1561,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   h->NP = t->n_points;
   // measured: row-marching DFMA for 2-D, tensor cores for 3-D
   h->engine = cfg->dim == 2 ? 4 : 2;
-  h->kz = cfg->dim == 2 ? 8 : (cfg->radius == 3 ? 32 : 16);
+  h->kz = cfg->dim == 2 ? 8 : 32;  // 3-D R=2: 32 measured 0.4 % faster than 16 (configs 3, 4)
   if (dist) {
     h->rank = dist->rank;
     h->nranks = dist->nranks;
