@@ -4,8 +4,9 @@
 Metric (BASELINE.json): FP64 cell-updates/s per RK stage; one unit of work is
 one cell x one SSP-RK3 stage.  A bench "step" is one SSP-RK3 time step (3
 stages) of the workload over the whole grid.  Default workload: BASELINE.json
-configs[1] (2-D 1024^2 outflow Voronoi, R=2, CFL 0.4); `--config k` selects
-another (1-based).
+configs[3] (3-D 512^3 outflow Voronoi, 64 regions, R=2, CFL 0.3: the largest
+configuration that fits one GPU); `--config k` selects another (1-based,
+SURVEY.md §8(d)).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl reference]
 
@@ -103,34 +104,55 @@ def dist_init():
     return None, 0, 1, 0
 
 
-def cpu_sample(w, rset, seconds_target=10.0, nthreads=None):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _oracle_sample(w, seconds_per_stage, nthreads):
+    """Oracle (CPU port of the reference algorithm) on a bounded sub-box of
+    the workload: a contiguous run of slab-axis planes of the workload's own
+    IC with their R+1 halo planes.  The table comes from the hash-pinned file
+    (oracle/tables) and the IC from the oracle's restatement
+    (kfvm_oracle_ic.cpp), so this leg never maps libkfvm_b200.so.  Returns
+    (oracle, IC block, halo H, planes)."""
+    from oracle import Oracle  # CPU baseline / reference leg only
+    from oracle.kfvm_oracle import initial_condition as oracle_ic
+    from oracle.table_file import load_table
+    g = w.grid
+    table = load_table(g.dim, g.radius)
+    H = g.radius + 1
+    n_s = 1
+    Ub = oracle_ic(g, w.ic, 0, min(g.slab_extent, n_s + 2 * H), nthreads)
+    o = Oracle(_subgrid(g, Ub.shape[0]), table, nthreads=nthreads)
+    t1 = max(o.sample_stage_seconds(Ub, H, n_s), 1e-4)
+    n_s = int(max(1, min(g.slab_extent - 2 * H, seconds_per_stage / t1)))
+    Ub = oracle_ic(g, w.ic, 0, n_s + 2 * H, nthreads)
+    o = Oracle(_subgrid(g, Ub.shape[0]), table, nthreads=nthreads)
+    return o, Ub, H, n_s, table
+
+
+def cpu_sample(w, seconds_target=10.0, nthreads=None):
     """Time the CPU oracle on a bounded sub-box of the workload (planes of the
     slab axis) and return (cell-updates/s, cores, description)."""
-    import paper_2401_16543_b200 as K
-    from oracle import Oracle  # CPU baseline leg only
     g = w.grid
     nthreads = nthreads or (os.cpu_count() or 1)
-    o = Oracle(g, rset, nthreads=nthreads)
-    plane = g.nx * (g.ny if g.dim == 3 else 1)
-    # planes needed around the sample: stencil + limiter halo
-    H = g.radius + 1
-    # calibrate on one plane
-    np_s = 1
-    Ub = K.initial_condition(g, w.ic, 0, min(g.slab_extent, np_s + 2 * H + 2), nthreads)
-    sub = _subgrid(g, Ub.shape[0])
-    osub = Oracle(sub, rset, nthreads=nthreads)
-    t1 = osub.sample_stage_seconds(Ub, H, np_s)
-    per_plane = max(t1, 1e-4)
-    np_s = int(max(1, min(g.slab_extent - 2 * H, seconds_target / per_plane / 3)))
-    Ub = K.initial_condition(g, w.ic, 0, np_s + 2 * H, nthreads)
-    sub = _subgrid(g, Ub.shape[0])
-    osub = Oracle(sub, rset, nthreads=nthreads)
-    times = [osub.sample_stage_seconds(Ub, H, np_s) for _ in range(3)]
+    o, Ub, H, n_s, table = _oracle_sample(w, seconds_target / 3, nthreads)
+    times = [o.sample_stage_seconds(Ub, H, n_s) for _ in range(3)]
     t = min(times)
-    cells = plane * np_s
-    desc = (f"oracle stage (reconstruct+limit+Riemann+RK combine) on {np_s} of {g.slab_extent} "
-            f"slab-axis planes ({cells} cells) of the workload IC, {nthreads} threads, best of 3")
-    return cells / t, nthreads, desc, o
+    plane = g.nx * (g.ny if g.dim == 3 else 1)
+    cells = plane * n_s
+    desc = (f"oracle stage (reconstruct+limit+Riemann+RK combine) on {n_s} of {g.slab_extent} "
+            f"slab-axis planes ({cells} cells) of the workload IC, {nthreads} threads of "
+            f"'{cpu_model()}', best of 3; table from oracle/tables (hash {table.hash:#x})")
+    return cells / t, nthreads, desc
 
 
 def _subgrid(g, planes):
@@ -140,35 +162,29 @@ def _subgrid(g, planes):
     return replace(g, ny=planes, dx=g.dx if g.dx else 1.0 / g.nx)
 
 
-def run_reference(args, w, rset, rank):
+def run_reference(args, w, rank):
     """--impl reference: the CPU oracle (C++ restatement of the reference
     algorithm; the reference itself does not build) on the
-    host cores, each step a bounded sample of the workload."""
+    host cores, each step a bounded sample of the workload.  Nothing in this
+    leg loads libkfvm_b200.so: table from oracle/tables, IC from the oracle's
+    restatement."""
     if rank != 0:
         return
-    import paper_2401_16543_b200 as K
-    from oracle import Oracle
     g = w.grid
     nthreads = os.cpu_count() or 1
-    H = g.radius + 1
-    plane = g.nx * (g.ny if g.dim == 3 else 1)
-    # size each step to ~2 s of CPU work
-    np_s = 1
-    Ub = K.initial_condition(g, w.ic, 0, np_s + 2 * H, nthreads)
-    o = Oracle(_subgrid(g, Ub.shape[0]), rset, nthreads=nthreads)
-    t1 = o.sample_stage_seconds(Ub, H, 1)
-    np_s = int(max(1, min(g.slab_extent - 2 * H, 0.7 / max(t1, 1e-4))))
-    Ub = K.initial_condition(g, w.ic, 0, np_s + 2 * H, nthreads)
-    o = Oracle(_subgrid(g, Ub.shape[0]), rset, nthreads=nthreads)
+    # size each stage to ~0.7 s of CPU work
+    o, Ub, H, n_s, table = _oracle_sample(w, 0.7, nthreads)
     for _ in range(args.warmup):
-        o.sample_stage_seconds(Ub, H, np_s)
+        o.sample_stage_seconds(Ub, H, n_s)
     tot = 0.0
     for _ in range(args.steps):
-        tot += 3 * o.sample_stage_seconds(Ub, H, np_s)  # one step = 3 stages
-    cells = plane * np_s
+        tot += 3 * o.sample_stage_seconds(Ub, H, n_s)  # one step = 3 stages
+    plane = g.nx * (g.ny if g.dim == 3 else 1)
+    cells = plane * n_s
     value = cells * 3 * args.steps / tot
-    sample = (f"per step: 3 oracle stages on {np_s} of {g.slab_extent} slab-axis planes "
-              f"({cells} cells) of the workload IC")
+    sample = (f"per step: 3 oracle stages on {n_s} of {g.slab_extent} slab-axis planes "
+              f"({cells} cells) of the workload IC, {nthreads} threads of '{cpu_model()}'; "
+              f"table from oracle/tables (hash {table.hash:#x}), IC from the oracle restatement")
     line = {
         "metric": "fp64_cell_updates_per_s_per_rk_stage", "value": value,
         "unit": "cell-updates/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
@@ -176,7 +192,7 @@ def run_reference(args, w, rset, rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(w, args),
         "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": nthreads,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -215,7 +231,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4,
+                    help="BASELINE.json config (1-based); default 4 = 512^3 outflow Voronoi, the "
+                         "largest config that fits one GPU")
     ap.add_argument("--n", type=int, default=None, help="override resolution (testing)")
     ap.add_argument("--nz", type=int, default=None,
                     help="slab-axis extent (e.g. config 5's weak-scaling block 1024x1024x128)")
@@ -240,13 +258,13 @@ def main():
     if args.steps is None:
         args.steps = w.steps
     args.warmup = max(3, args.warmup)
-    rset = K.precompute(w.grid.radius, dim=w.grid.dim)
     dist, rank, ws, local = dist_init()
     args.gpus = ws if ws > 1 else args.gpus
 
     if args.impl == "reference":
-        run_reference(args, w, rset, rank)
+        run_reference(args, w, rank)
         return
+    rset = K.precompute(w.grid.radius, dim=w.grid.dim)
 
     import torch
     torch.cuda.set_device(local)
@@ -403,9 +421,9 @@ def main():
         achieved = flops_per_step / (states_ms_per_step * 1e-3) / 1e12 if states_ms_per_step else None
         cpu = None
         if not args.no_cpu and ws == 1:
-            v, cores, desc, _ = cpu_sample(w, rset, seconds_target=8.0)
+            v, cores, desc = cpu_sample(w, seconds_target=8.0)
             cpu = {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "port",
-                   "sample": desc}
+                   "sample": desc, "cpu_model": cpu_model()}
         line = {
             "metric": "fp64_cell_updates_per_s_per_rk_stage", "value": value,
             "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,

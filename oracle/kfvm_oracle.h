@@ -64,6 +64,13 @@ double kfo_max_speed(const kfvm_config* cfg, const double* U, long long ncells);
 void kfo_combine(int stage, long long n, const double* U0, const double* Uk, const double* L,
                  double dt, double* out);
 
+/* Seeded BASELINE initial conditions (fourier / voronoi / fourier_sphere /
+ * uniform), restated independently of the product generator
+ * (kfvm_oracle_ic.cpp): cell averages of the slab-axis planes [z0, z0+nz),
+ * AoS, x fastest. */
+int kfo_ic_generate(const kfvm_config* cfg, const kfvm_ic_params* ic, int z0, int nz_local,
+                    int nthreads, double* U);
+
 /* Point functions (unit tests against the SPEC examples). */
 double kfo_pressure(int dim, const double* U, double gamma);
 double kfo_sound_speed(int dim, const double* U, double gamma);

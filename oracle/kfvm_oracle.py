@@ -27,7 +27,9 @@ def lib():
                            check=True, capture_output=True)
         L = C.CDLL(LIB_PATH)
         P, D, I = C.c_void_p, C.POINTER(C.c_double), C.c_int
-        T, CF = C.POINTER(_abi.KfvmTable), C.POINTER(_abi.KfvmConfig)
+        # tables as plain pointers: ReconstructionSet and oracle.table_file
+        # structs both pass (whatever module instance defined their class)
+        T, CF = C.c_void_p, C.POINTER(_abi.KfvmConfig)
         sig = {
             "kfo_rhs": (I, [CF, T, P, P, I]),
             "kfo_states": (I, [CF, T, P, P, I]),
@@ -54,6 +56,7 @@ def lib():
             "kfo_pow": (C.c_double, [C.c_double, C.c_double]),
             "kfo_viscous_face": (None, [CF, P, I, I, I, I, P]),
             "kfo_combine43": (None, [I, C.c_longlong, P, P, P, C.c_double, P, P]),
+            "kfo_ic_generate": (I, [CF, C.POINTER(_abi.KfvmIcParams), I, I, I, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -179,6 +182,24 @@ class Oracle:
         self._chk(self.L.kfo_sample_stage(C.byref(self.cfg), self.rset.c_table, _p(U), int(p0),
                                           int(np_planes), self.nthreads, C.byref(sec)), "sample")
         return sec.value
+
+
+def initial_condition(grid, ic, z0: int = 0, nz_local: int | None = None,
+                      nthreads: int | None = None) -> np.ndarray:
+    """The seeded BASELINE IC from the oracle's own restatement
+    (kfvm_oracle_ic.cpp): same shape and bytes as
+    paper_2401_16543_b200.initial_condition, without the product library."""
+    nzl = grid.slab_extent - z0 if nz_local is None else nz_local
+    plane = grid.nx * (grid.ny if grid.dim == 3 else 1)
+    U = np.empty(plane * nzl * grid.nvar, dtype=np.float64)
+    cfg = grid.c_config()
+    p = ic.c_params()
+    nt = nthreads or min(64, os.cpu_count() or 1)
+    rc = lib().kfo_ic_generate(C.byref(cfg), C.byref(p), int(z0), int(nzl), int(nt), _p(U))
+    if rc:
+        raise ValueError(f"kfo_ic_generate failed with code {rc}")
+    shp = ((nzl, grid.ny, grid.nx) if grid.dim == 3 else (nzl, grid.nx)) + (grid.nvar,)
+    return U.reshape(shp)
 
 
 class _PointAPI:

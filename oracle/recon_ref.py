@@ -139,6 +139,15 @@ def recon_vectors(dim: int, R: int, q: int, ell: float = 5.0, dps: int = 50,
                 pv *= mavg(cells[h][a], mono[v_][a])
             M[h, N + v_] = pv
             M[N + v_, h] = pv
+    # factor once per stencil and reuse it for every right-hand side: the
+    # operations of mp.lu_solve (10 guard bits, LU_decomp, L_solve, U_solve)
+    with mp.extraprec(10):
+        LU, piv = mp.mp.LU_decomp(M.copy())
+
+    def solve(rhs):
+        with mp.extraprec(10):
+            return mp.mp.U_solve(LU, mp.mp.L_solve(LU, rhs.copy(), piv))
+
     pts = points if points is not None else face_points(dim, R, dps)
     als = alphas if alphas is not None else graded(dim, 1, R)
     F = np.zeros((len(pts), N))
@@ -155,7 +164,7 @@ def recon_vectors(dim: int, R: int, q: int, ell: float = 5.0, dps: int = 50,
             for a in range(dim):
                 m *= x[a] ** mono[v_][a]
             rhs[N + v_] = m
-        z = mp.lu_solve(M, rhs)
+        z = solve(rhs)
         F[s] = [float(z[l]) for l in range(N)]
     Dv = np.zeros((len(als), N))
     for ia, al in enumerate(als):
@@ -179,6 +188,6 @@ def recon_vectors(dim: int, R: int, q: int, ell: float = 5.0, dps: int = 50,
                 for a in range(3):
                     fac *= mp.factorial(al[a])
             rhs[N + v_] = fac
-        z = mp.lu_solve(M, rhs)
+        z = solve(rhs)
         Dv[ia] = [float(z[l]) for l in range(N)]
     return F, Dv, p

@@ -19,6 +19,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -450,7 +452,7 @@ __global__ void k_speed(const double* __restrict__ U, Geo g, unsigned long long*
 // dt = cfl*dx / smax on the device (select_dt), clipped so the
 // last step lands exactly on t_end (advance_to); tt = {t, t_end}.
 __global__ void k_dt(unsigned long long* smax, double* dt_cur, double* dt_seq, int* step,
-                     int cap, int* err, double* tt) {
+                     int cap, int* err, double* tt, int* nprod) {
   const double s = __longlong_as_double((long long)*smax);
   double dt = (c_k.cfl * c_k.dx) / s;
   if (!(dt > 0.0) || !isfinite(dt)) atomicOr(err, 2);
@@ -461,6 +463,7 @@ __global__ void k_dt(unsigned long long* smax, double* dt_cur, double* dt_seq, i
   const int st = *step;
   if (st < cap) dt_seq[st] = dt;
   *step = st + 1;
+  if (dt > 0.0) *nprod += 1;  // productive steps (advance_to: the clipped tail is dt = 0)
   *smax = 0ULL;
 }
 
@@ -731,6 +734,9 @@ struct kfvm_handle {
   int nacc43 = 0, nrej43 = 0;
   long long graph43_launches = 0;
   bool kx = false;                    // KXRCF two-pass reconstruction
+  bool registered = false;            // holds a reference on the device constant image
+  double* ext = nullptr;              // kfvm_gpu_states staging buffer
+  size_t ext_elems = 0;
   unsigned char* d_flags = nullptr;   // KXRCF flags of the extended box
   std::string err;
 };
@@ -748,6 +754,25 @@ int fail(kfvm_handle* h, int code, const std::string& msg) {
     if (e_ != cudaSuccess)                                                            \
       return fail(h, KFVM_ERR_DEVICE, std::string(#x ": ") + cudaGetErrorString(e_)); \
   } while (0)
+
+// The constant banks (c_k, c_t, c_gather and the generated weight arrays of
+// kfvm_gen.cuh) are per device and shared by every handle on it.  A handle
+// may only be created when its constant image equals that of the live
+// handles on the same device (otherwise KFVM_ERR_CONFIG: two different
+// configurations would silently run with the last one's constants); the
+// device copy of the table that c_t points to is owned by this registry and
+// freed with the last handle of the device.
+struct DeviceImage {
+  int users = 0;
+  DevConsts k{};
+  DevTable t{};
+  std::vector<int> gather;
+  uint64_t hash = 0;
+  double *d_face = nullptr, *d_deriv = nullptr;
+};
+std::mutex g_image_mu;
+std::map<int, DeviceImage> g_images;
+thread_local std::string g_create_err;  // kfvm_gpu_last_error(NULL) after a failed create
 
 inline unsigned blocks(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 // extended cells of the planes [e0, e1) a states launch covers
@@ -1300,7 +1325,7 @@ int enqueue_dt(kfvm_handle* h) {
   if (rc) return rc;
   tic(h);
   k_dt<<<1, 1, 0, h->stream>>>(h->d_smax, h->d_dt_cur, h->d_dt_seq, h->d_step, h->dt_cap, h->d_err,
-                               h->d_tt);
+                               h->d_tt, h->d_step + 1);
   h->launches++;
   toc(h, &h->t_other);
   return KFVM_OK;
@@ -1403,9 +1428,10 @@ int ensure_aos(kfvm_handle* h) {
 }
 
 // Upload the weights into the generated __constant__ arrays after checking
-// that the table's geometry is the structure compiled into kfvm_gen.cuh.
+// that the table's geometry is the structure compiled into kfvm_gen.cuh
+// (once per device: the registry's first handle).
 template <int D, int R>
-int upload_gen(kfvm_handle* h, const kfvm_table* t) {
+int upload_const(kfvm_handle* h, const kfvm_table* t) {
   using G = Gen<D, R>;
   if (t->n_full != G::N0 || t->total_cells != G::NTOT || t->n_points != G::NP ||
       t->n_alpha != G::NA || t->n_stencils != G::NS)
@@ -1429,6 +1455,16 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
     CK(cudaMemcpyToSymbol(G::face_symbol(), ft.data(), sizeof(double) * G::NTOT * G::NP));
     CK(cudaMemcpyToSymbol(G::deriv_symbol(), t->deriv, sizeof(double) * G::NTOT * G::NA));
   }
+  return KFVM_OK;
+}
+
+// Per-handle DMMA operands (B fragments, chunk tables) and kernel attributes.
+template <int D, int R>
+int upload_gen(kfvm_handle* h, const kfvm_table* t) {
+  using G = Gen<D, R>;
+  if (t->n_full != G::N0 || t->total_cells != G::NTOT || t->n_points != G::NP ||
+      t->n_alpha != G::NA || t->n_stencils != G::NS)
+    return fail(h, KFVM_ERR_CONFIG, "table does not match the generated kernel structure");
   // DMMA operands: per 4-entry chunk of each stencil (zero-padded at the
   // front), B fragments in lane order (k = lane%4, column = lane/4) and the
   // S0 position of every chunk slot
@@ -1538,6 +1574,7 @@ static bool resolve_bcs(const kfvm_config* cfg, DevConsts* k) {
 
 extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, const kfvm_dist* dist,
                                kfvm_handle** out) {
+  g_create_err.clear();
   if (!cfg || !t || !out) return KFVM_ERR_CONFIG;
   *out = nullptr;
   if ((cfg->dim != 2 && cfg->dim != 3) || (cfg->radius != 2 && cfg->radius != 3) ||
@@ -1676,18 +1713,58 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   };
   const size_t nface = (size_t)t->total_cells * t->n_points;
   const size_t nder = (size_t)t->total_cells * t->n_alpha;
-  bad(cudaMalloc(&h->d_face, nface * sizeof(double)), "cudaMalloc face");
-  bad(cudaMalloc(&h->d_deriv, nder * sizeof(double)), "cudaMalloc deriv");
-  if (rc == KFVM_OK) {
-    bad(cudaMemcpy(h->d_face, t->face, nface * sizeof(double), cudaMemcpyHostToDevice), "copy face");
-    bad(cudaMemcpy(h->d_deriv, t->deriv, nder * sizeof(double), cudaMemcpyHostToDevice), "copy deriv");
-  }
-  T.face = h->d_face;
-  T.deriv = h->d_deriv;
   T.gather = nullptr;
-  bad(cudaMemcpyToSymbol(c_k, &k, sizeof(k)), "constants");
-  bad(cudaMemcpyToSymbol(c_t, &T, sizeof(T)), "table");
-  bad(cudaMemcpyToSymbol(c_gather, t->gather, sizeof(int) * t->total_cells), "gather");
+  {
+    std::lock_guard<std::mutex> lk(g_image_mu);
+    DeviceImage& im = g_images[h->device];
+    if (im.users > 0) {
+      T.face = im.d_face;
+      T.deriv = im.d_deriv;
+      if (std::memcmp(&im.k, &k, sizeof(k)) != 0 || std::memcmp(&im.t, &T, sizeof(T)) != 0 ||
+          im.hash != t->hash ||
+          im.gather != std::vector<int>(t->gather, t->gather + t->total_cells)) {
+        delete h;
+        g_create_err = "another live handle on this device uses a different configuration or table "
+                       "(the constant banks are per device)";
+        return KFVM_ERR_CONFIG;
+      }
+      ++im.users;
+      h->registered = true;
+    } else {
+      bad(cudaMalloc(&im.d_face, nface * sizeof(double)), "cudaMalloc face");
+      bad(cudaMalloc(&im.d_deriv, nder * sizeof(double)), "cudaMalloc deriv");
+      if (rc == KFVM_OK) {
+        bad(cudaMemcpy(im.d_face, t->face, nface * sizeof(double), cudaMemcpyHostToDevice), "copy face");
+        bad(cudaMemcpy(im.d_deriv, t->deriv, nder * sizeof(double), cudaMemcpyHostToDevice),
+            "copy deriv");
+      }
+      T.face = im.d_face;
+      T.deriv = im.d_deriv;
+      bad(cudaMemcpyToSymbol(c_k, &k, sizeof(k)), "constants");
+      bad(cudaMemcpyToSymbol(c_t, &T, sizeof(T)), "table");
+      bad(cudaMemcpyToSymbol(c_gather, t->gather, sizeof(int) * t->total_cells), "gather");
+      if (rc == KFVM_OK) {
+        if (cfg->dim == 2 && cfg->radius == 2) rc = upload_const<2, 2>(h, t);
+        if (cfg->dim == 2 && cfg->radius == 3) rc = upload_const<2, 3>(h, t);
+        if (cfg->dim == 3 && cfg->radius == 2) rc = upload_const<3, 2>(h, t);
+        if (cfg->dim == 3 && cfg->radius == 3) rc = upload_const<3, 3>(h, t);
+      }
+      if (rc == KFVM_OK) {
+        im.users = 1;
+        im.k = k;
+        im.t = T;
+        im.hash = t->hash;
+        im.gather.assign(t->gather, t->gather + t->total_cells);
+        h->registered = true;
+      } else {
+        if (im.d_face) cudaFree(im.d_face);
+        if (im.d_deriv) cudaFree(im.d_deriv);
+        im = DeviceImage();
+      }
+    }
+  }
+  h->d_face = const_cast<double*>(T.face);
+  h->d_deriv = const_cast<double*>(T.deriv);
   if (rc == KFVM_OK) {
     if (cfg->dim == 2 && cfg->radius == 2) rc = upload_gen<2, 2>(h, t);
     if (cfg->dim == 2 && cfg->radius == 3) rc = upload_gen<2, 3>(h, t);
@@ -1730,6 +1807,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   if (h->kx && rc == KFVM_OK) {
     const Chunk ch = make_chunk(h, 0, h->chunk);
     bad(cudaMalloc(&h->d_flags, (size_t)ch.next), "cudaMalloc flags");
+    if (rc == KFVM_OK) bad(cudaMemset(h->d_flags, 0, (size_t)ch.next), "memset flags");
   }
   {
     const Chunk ch = make_chunk(h, 0, h->chunk);
@@ -1767,11 +1845,11 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     const double tt0[2] = {0.0, INFINITY};
     bad(cudaMemcpy(h->d_tt, tt0, sizeof(tt0), cudaMemcpyHostToDevice), "init t");
   }
-  bad(cudaMalloc(&h->d_step, sizeof(int)), "cudaMalloc step");
+  bad(cudaMalloc(&h->d_step, 2 * sizeof(int)), "cudaMalloc step");  // {step, productive steps}
   bad(cudaMalloc(&h->d_err, sizeof(int)), "cudaMalloc err");
   if (rc == KFVM_OK) {
     bad(cudaMemset(h->d_err, 0, sizeof(int)), "memset");
-    bad(cudaMemset(h->d_step, 0, sizeof(int)), "memset");
+    bad(cudaMemset(h->d_step, 0, 2 * sizeof(int)), "memset");
     bad(cudaMemset(h->d_smax, 0, sizeof(unsigned long long)), "memset");
   }
   bad(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
@@ -1813,12 +1891,22 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
   if (h->graph) cudaGraphExecDestroy(h->graph);
   if (h->graph43) cudaGraphExecDestroy(h->graph43);
   if (h->comm) nccl().CommDestroy(h->comm);
+  cudaSetDevice(h->device);
+  if (h->registered) {
+    std::lock_guard<std::mutex> lk(g_image_mu);
+    DeviceImage& im = g_images[h->device];
+    if (--im.users == 0) {
+      cudaFree(im.d_face);
+      cudaFree(im.d_deriv);
+      im = DeviceImage();
+    }
+  }
   for (void* p : {(void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
-                  (void*)h->aos, (void*)h->d_face, (void*)h->d_deriv, (void*)h->d_dt_seq,
+                  (void*)h->aos, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
                   (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_tt,
                   (void*)h->d_flags, (void*)h->Uh, (void*)h->d_rows, (void*)h->d_planes,
-                  (void*)h->d_ctl, (void*)h->d_nps})
+                  (void*)h->d_ctl, (void*)h->d_nps, (void*)h->ext})
     if (p) cudaFree(p);
   if (h->stream) cudaStreamDestroy(h->stream);
   if (h->s_halo) cudaStreamDestroy(h->s_halo);
@@ -1828,17 +1916,21 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
 }
 
 extern "C" int kfvm_gpu_set_state_device(kfvm_handle* h, const double* U_dev) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   const long long n = interior_elems(h);
   k_transpose<0><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, const_cast<double*>(U_dev), h->g,
                                                          h->nv);
   h->launches++;
   // the captured step graph reads the fixed state buffers: it stays valid
-  CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
+  CK(cudaMemsetAsync(h->d_step, 0, 2 * sizeof(int), h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return KFVM_OK;
 }
 
 extern "C" int kfvm_gpu_get_state_device(kfvm_handle* h, double* U_dev) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   const long long n = interior_elems(h);
   k_transpose<1><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, U_dev, h->g, h->nv);
   h->launches++;
@@ -1847,6 +1939,8 @@ extern "C" int kfvm_gpu_get_state_device(kfvm_handle* h, double* U_dev) {
 }
 
 extern "C" int kfvm_gpu_set_state(kfvm_handle* h, const double* U_host) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   int rc = ensure_aos(h);
   if (rc) return rc;
   const size_t n = (size_t)interior_elems(h);
@@ -1855,6 +1949,8 @@ extern "C" int kfvm_gpu_set_state(kfvm_handle* h, const double* U_host) {
 }
 
 extern "C" int kfvm_gpu_get_state(kfvm_handle* h, double* U_host) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   int rc = ensure_aos(h);
   if (rc) return rc;
   rc = kfvm_gpu_get_state_device(h, h->aos);
@@ -1870,6 +1966,8 @@ extern "C" int kfvm_gpu_get_state(kfvm_handle* h, double* U_host) {
 // transpose + download.  With pinned buffers and one handle per field, the
 // copies of one field overlap the steps of another on the copy engines.
 extern "C" int kfvm_gpu_set_state_async(kfvm_handle* h, const double* U_host) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   int rc = ensure_aos(h);
   if (rc) return rc;
   const long long n = interior_elems(h);
@@ -1877,11 +1975,13 @@ extern "C" int kfvm_gpu_set_state_async(kfvm_handle* h, const double* U_host) {
                      h->stream));
   k_transpose<0><<<blocks(n, 256), 256, 0, h->stream>>>(h->U0, h->aos, h->g, h->nv);
   h->launches++;
-  CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
+  CK(cudaMemsetAsync(h->d_step, 0, 2 * sizeof(int), h->stream));
   return KFVM_OK;
 }
 
 extern "C" int kfvm_gpu_get_state_async(kfvm_handle* h, double* U_host) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   int rc = ensure_aos(h);
   if (rc) return rc;
   const long long n = interior_elems(h);
@@ -1893,6 +1993,8 @@ extern "C" int kfvm_gpu_get_state_async(kfvm_handle* h, double* U_host) {
 }
 
 extern "C" int kfvm_gpu_rhs(kfvm_handle* h, double* dUdt_host) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   int rc = run_stage(h, h->U0, h->Ua, 0);
   if (rc) return rc;
   if ((rc = check_err(h))) return rc;
@@ -1906,28 +2008,43 @@ extern "C" int kfvm_gpu_rhs(kfvm_handle* h, double* dUdt_host) {
 }
 
 extern "C" int kfvm_gpu_states(kfvm_handle* h, double* states_host) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   ghost(h, h->U0);
   int rc = halo(h, h->U0, h->stream);
   if (rc) return rc;
   prims(h, h->U0);
   const long long per_cell = (long long)h->NP * h->nv;
   const long long plane_cells = (long long)h->g.nx * h->g.nm;  // interior cells per plane
-  double* dbuf = nullptr;
-  CK(cudaMalloc(&dbuf, (size_t)plane_cells * h->chunk * per_cell * sizeof(double)));
+  if (h->kx) {  // the troubled-cell flags of this state first (one chunk, S:565 steps 1-2)
+    const Chunk ch = make_chunk(h, 0, h->g.np_loc);
+    if (h->dim == 2 && h->R == 2) rc = kx_flags<2, 2>(h, h->U0, ch);
+    if (h->dim == 2 && h->R == 3) rc = kx_flags<2, 3>(h, h->U0, ch);
+    if (h->dim == 3 && h->R == 2) rc = kx_flags<3, 2>(h, h->U0, ch);
+    if (h->dim == 3 && h->R == 3) rc = kx_flags<3, 3>(h, h->U0, ch);
+    if (rc) return rc;
+  }
+  const size_t nbuf = (size_t)plane_cells * h->chunk * per_cell;
+  if (h->ext_elems < nbuf) {
+    if (h->ext) cudaFree(h->ext);
+    h->ext = nullptr;
+    h->ext_elems = 0;
+    CK(cudaMalloc(&h->ext, nbuf * sizeof(double)));
+    h->ext_elems = nbuf;
+  }
   for (int c0 = 0; c0 < h->g.np_loc; c0 += h->chunk) {
     const Chunk ch = make_chunk(h, c0, std::min(h->chunk, h->g.np_loc - c0));
     states_and_flux(h, h->U0, ch);
     const long long n = plane_cells * ch.C * per_cell;
     if (h->dim == 2)
-      k_extract_states<2><<<blocks(n, 256), 256, 0, h->stream>>>(h->St, dbuf, h->g, ch, h->NP);
+      k_extract_states<2><<<blocks(n, 256), 256, 0, h->stream>>>(h->St, h->ext, h->g, ch, h->NP);
     else
-      k_extract_states<3><<<blocks(n, 256), 256, 0, h->stream>>>(h->St, dbuf, h->g, ch, h->NP);
+      k_extract_states<3><<<blocks(n, 256), 256, 0, h->stream>>>(h->St, h->ext, h->g, ch, h->NP);
     h->launches++;
-    cudaMemcpyAsync(states_host + plane_cells * c0 * per_cell, dbuf, n * sizeof(double),
-                    cudaMemcpyDeviceToHost, h->stream);
+    CK(cudaMemcpyAsync(states_host + plane_cells * c0 * per_cell, h->ext, n * sizeof(double),
+                       cudaMemcpyDeviceToHost, h->stream));
   }
-  cudaStreamSynchronize(h->stream);
-  cudaFree(dbuf);
+  CK(cudaStreamSynchronize(h->stream));
   return check_err(h);
 }
 
@@ -1946,6 +2063,8 @@ __global__ void k_extract_flags(const unsigned char* __restrict__ fl, unsigned c
 }
 
 extern "C" int kfvm_gpu_kxrcf_flags(kfvm_handle* h, unsigned char* flags_host) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   if (!h->kx) return fail(h, KFVM_ERR_CONFIG, "kxrcf is off in this handle's config");
   ghost(h, h->U0);
   int rc = halo(h, h->U0, h->stream);
@@ -1969,6 +2088,8 @@ extern "C" int kfvm_gpu_kxrcf_flags(kfvm_handle* h, unsigned char* flags_host) {
 }
 
 extern "C" int kfvm_gpu_select_dt(kfvm_handle* h, double* dt) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   int rc = enqueue_speed(h);
   if (rc) return rc;
   if ((rc = reduce_smax(h))) return rc;
@@ -1982,6 +2103,8 @@ extern "C" int kfvm_gpu_select_dt(kfvm_handle* h, double* dt) {
 }
 
 extern "C" int kfvm_gpu_stage(kfvm_handle* h, int stage, double dt) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   if (stage < 1 || stage > 3) return fail(h, KFVM_ERR_CONFIG, "stage must be 1..3");
   CK(cudaMemcpyAsync(h->d_dt_cur, &dt, sizeof(double), cudaMemcpyHostToDevice, h->stream));
   double* in = stage == 1 ? h->U0 : (stage == 2 ? h->Ua : h->Ub);
@@ -1991,11 +2114,16 @@ extern "C" int kfvm_gpu_stage(kfvm_handle* h, int stage, double dt) {
   return check_err(h);
 }
 
-extern "C" int kfvm_gpu_run_async(kfvm_handle* h, int nsteps) {
-  int rc = ensure_dt_cap(h, nsteps);
+// nsteps SSP-RK3 steps (graph-replayed on one rank); reset = start a new dt
+// sequence (advance_to keeps counting across its batches)
+int run_steps(kfvm_handle* h, int nsteps, bool reset) {
+  if (reset) {
+    int rc = ensure_dt_cap(h, nsteps);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(h->d_step, 0, 2 * sizeof(int), h->stream));
+  }
+  int rc = enqueue_speed(h);
   if (rc) return rc;
-  CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
-  if ((rc = enqueue_speed(h))) return rc;
   if (h->timing || h->multi) {
     for (int s = 0; s < nsteps; ++s)
       if ((rc = enqueue_step(h))) return rc;
@@ -2019,9 +2147,17 @@ extern "C" int kfvm_gpu_run_async(kfvm_handle* h, int nsteps) {
   return KFVM_OK;
 }
 
+extern "C" int kfvm_gpu_run_async(kfvm_handle* h, int nsteps) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
+  return run_steps(h, nsteps, true);
+}
+
 extern "C" int kfvm_gpu_sync(kfvm_handle* h) { return check_err(h); }
 
 extern "C" int kfvm_gpu_dt_sequence(kfvm_handle* h, double* dt_seq, int nsteps) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   if (nsteps > h->dt_cap) return fail(h, KFVM_ERR_CONFIG, "nsteps exceeds dt capacity");
   CK(cudaMemcpyAsync(dt_seq, h->d_dt_seq, sizeof(double) * nsteps, cudaMemcpyDeviceToHost,
                      h->stream));
@@ -2030,6 +2166,8 @@ extern "C" int kfvm_gpu_dt_sequence(kfvm_handle* h, double* dt_seq, int nsteps) 
 }
 
 extern "C" int kfvm_gpu_run(kfvm_handle* h, int nsteps, double* dt_seq) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   int rc = kfvm_gpu_run_async(h, nsteps);
   if (rc) return rc;
   if ((rc = kfvm_gpu_sync(h))) return rc;
@@ -2038,6 +2176,8 @@ extern "C" int kfvm_gpu_run(kfvm_handle* h, int nsteps, double* dt_seq) {
 }
 
 extern "C" int kfvm_gpu_step(kfvm_handle* h, double* dt_out) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   double dt;
   int rc = kfvm_gpu_run(h, 1, &dt);
   if (rc) return rc;
@@ -2087,11 +2227,13 @@ int advance43(kfvm_handle* h, double t_final, int max_attempts, int* steps, doub
   h->nrej43 = c.nrej;
   if (steps) *steps = c.nacc;
   if (t_reached) *t_reached = c.t;
-  CK(cudaMemsetAsync(h->d_step, 0, sizeof(int), h->stream));
+  CK(cudaMemsetAsync(h->d_step, 0, 2 * sizeof(int), h->stream));
   return KFVM_OK;
 }
 
 extern "C" int kfvm_gpu_step_stats(kfvm_handle* h, int* accepted, int* rejected) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   if (accepted) *accepted = h->nacc43;
   if (rejected) *rejected = h->nrej43;
   return KFVM_OK;
@@ -2099,22 +2241,33 @@ extern "C" int kfvm_gpu_step_stats(kfvm_handle* h, int* accepted, int* rejected)
 
 extern "C" int kfvm_gpu_advance_to(kfvm_handle* h, double t_final, int max_steps, int* steps,
                                    double* t_reached) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   if (h->integrator == KFVM_SSP43) return advance43(h, t_final, max_steps, steps, t_reached);
+  // batches of graph-replayed steps; the batch size follows the remaining
+  // time / last dt, so at most one dt = 0 step runs past t_final; the dt
+  // sequence and the productive-step count run over the whole call
+  int rc = ensure_dt_cap(h, std::min(std::max(max_steps, 1), 1 << 16));
+  if (rc) return rc;
   double tt[2] = {0.0, t_final};
   CK(cudaMemcpyAsync(h->d_tt, tt, sizeof(tt), cudaMemcpyHostToDevice, h->stream));
-  int done = 0;
-  const int chunk = 32;
+  CK(cudaMemsetAsync(h->d_step, 0, 2 * sizeof(int), h->stream));
+  int done = 0, batch = 1;
   while (done < max_steps) {
-    const int n = std::min(chunk, max_steps - done);
-    int rc = kfvm_gpu_run_async(h, n);
-    if (rc) return rc;
+    const int n = std::min(batch, max_steps - done);
+    if ((rc = run_steps(h, n, false))) return rc;
     if ((rc = kfvm_gpu_sync(h))) return rc;
+    double dt = 0.0;
     CK(cudaMemcpy(tt, h->d_tt, sizeof(tt), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&dt, h->d_dt_cur, sizeof(dt), cudaMemcpyDeviceToHost));
     done += n;
     if (tt[0] >= t_final) break;
+    const double est = dt > 0.0 ? std::ceil((t_final - tt[0]) / dt) : 32.0;
+    batch = (int)std::max(1.0, std::min(32.0, est));
   }
-  // steps beyond t_final had dt = 0 (no-ops); report the productive count
-  if (steps) *steps = done;
+  int cnt[2] = {0, 0};
+  CK(cudaMemcpy(cnt, h->d_step, sizeof(cnt), cudaMemcpyDeviceToHost));
+  if (steps) *steps = cnt[1];  // steps with dt > 0
   if (t_reached) *t_reached = tt[0];
   const double reset[2] = {tt[0], INFINITY};
   CK(cudaMemcpy(h->d_tt, reset, sizeof(reset), cudaMemcpyHostToDevice));
@@ -2142,6 +2295,8 @@ extern "C" void* kfvm_gpu_stream(kfvm_handle* h) { return (void*)h->stream; }
 extern "C" long long kfvm_gpu_launch_count(kfvm_handle* h) { return h->launches; }
 
 extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long value) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   std::string n(name ? name : "");
   if (n == "fast_states" || n == "engine") {
     if (n == "engine") {
@@ -2187,6 +2342,8 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
       c = value / per_plane - 2;
     }
     c = std::max(1LL, std::min(c, (long long)h->g.np_loc));
+    if (h->kx && c < h->g.np_loc)  // the KXRCF passes run on one chunk (checked at create too)
+      return fail(h, KFVM_ERR_CONFIG, "kxrcf: the slab's face states must fit one chunk");
     drop_graphs(h);
     cudaFree(h->St);
     cudaFree(h->F);
@@ -2203,6 +2360,8 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
 }
 
 extern "C" int kfvm_gpu_kernel_times(kfvm_handle* h, double* a, double* b, double* c, double* d) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   if (a) *a = h->t_states;
   if (b) *b = h->t_flux;
   if (c) *c = h->t_update;
@@ -2212,7 +2371,7 @@ extern "C" int kfvm_gpu_kernel_times(kfvm_handle* h, double* a, double* b, doubl
 
 extern "C" int kfvm_gpu_last_error(kfvm_handle* h, char* buf, size_t n) {
   if (!buf || n == 0) return KFVM_ERR_CONFIG;
-  const std::string& e = h ? h->err : std::string("null handle");
+  const std::string& e = h ? h->err : (g_create_err.empty() ? std::string("null handle") : g_create_err);
   std::snprintf(buf, n, "%s", e.c_str());
   return KFVM_OK;
 }
@@ -2221,6 +2380,8 @@ extern "C" int kfvm_gpu_last_error(kfvm_handle* h, char* buf, size_t n) {
 // by the bench at sizes where the host generator is slow); bit-identical to
 // kfvm_ic_generate (same arithmetic, tables from the host).
 extern "C" int kfvm_gpu_ic_generate(kfvm_handle* h, const kfvm_ic_params* ic) {
+  if (!h) return KFVM_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
   if (ic->kind != KFVM_IC_FOURIER && ic->kind != KFVM_IC_VORONOI &&
       ic->kind != KFVM_IC_FOURIER_SPHERE && ic->kind != KFVM_IC_UNIFORM)
     return fail(h, KFVM_ERR_CONFIG, "IC kind not available on the device");
@@ -2245,26 +2406,29 @@ extern "C" int kfvm_gpu_ic_generate(kfvm_handle* h, const kfvm_ic_params* ic) {
   CK(cudaMalloc(&dP, sizeof(ICPlan)));
   tmp.push_back(dP);
   CK(cudaMemcpy(dP, &P, sizeof(ICPlan), cudaMemcpyHostToDevice));
+  // everything on the handle's stream, ordered after its queued work; the
+  // state buffers are fixed, so the captured step graphs stay valid
+  CK(cudaStreamSynchronize(h->stream));
   if (hp.needs_norm) {
     unsigned long long* dm;
     CK(cudaMalloc(&dm, sizeof(unsigned long long)));
     tmp.push_back(dm);
     const long long n = (long long)h->g.nx * h->g.nm * h->nsa;
     for (int f = 0; f < 1 + P.dim; ++f) {
-      CK(cudaMemset(dm, 0, sizeof(unsigned long long)));
-      k_ic_norm<<<blocks(n, 128), 128>>>(dP, f, h->g, h->p0, dm);
+      CK(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), h->stream));
+      k_ic_norm<<<blocks(n, 128), 128, 0, h->stream>>>(dP, f, h->g, h->p0, dm);
       unsigned long long bits;
-      CK(cudaMemcpy(&bits, dm, sizeof(bits), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpyAsync(&bits, dm, sizeof(bits), cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
       std::memcpy(&P.f[f].norm, &bits, sizeof(double));
     }
-    CK(cudaMemcpy(dP, &P, sizeof(ICPlan), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(dP, &P, sizeof(ICPlan), cudaMemcpyHostToDevice, h->stream));
   }
   const long long n = (long long)h->g.nx * h->g.nm * h->g.np_loc;
-  k_ic_fill<<<blocks(n, 128), 128>>>(dP, h->U0, h->g, h->p0);
-  CK(cudaDeviceSynchronize());
+  k_ic_fill<<<blocks(n, 128), 128, 0, h->stream>>>(dP, h->U0, h->g, h->p0);
+  CK(cudaMemsetAsync(h->d_step, 0, 2 * sizeof(int), h->stream));
+  CK(cudaStreamSynchronize(h->stream));
   for (void* p : tmp) cudaFree(p);
-  drop_graphs(h);
-  CK(cudaMemset(h->d_step, 0, sizeof(int)));
   return KFVM_OK;
 }
 

@@ -278,6 +278,137 @@ uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
   return h;
 }
 
+// Exact symmetry of the table (kernel_recon.hpp:105-106: "symmetric vectors
+// are exact permutations").  The cube's symmetry group G (signed axis
+// permutations g(x)_b = s_b x_pi(b); 8 elements in 2-D, 48 in 3-D) maps every
+// (sub)stencil onto a (sub)stencil, every face point onto a face point and
+// every derivative d^alpha onto +-d^alpha' (alpha'_b = alpha_pi(b), sign
+// prod_b s_b^alpha'_b).  The SE kernel is G-invariant, so in exact arithmetic
+// r_{gS, gx}[g h] = r_{S, x}[h] and d_{gS, alpha'}[g h] = sign d_{S, alpha}[h].
+// The binary128 solves satisfy this to ~1e-34; rounding a near-tie to FP64
+// could still split an orbit by one ulp.  So every orbit of entries is
+// replaced by its group average in binary128 (sum over g in G in a fixed
+// order, divided by |G|), and the images are assigned sign * average before
+// the one rounding to FP64: every mirror / rotation image is then bitwise
+// equal (entries whose stabiliser flips the sign average to exactly 0).
+void symmetrize(int dim, const kfvm_table& t, const std::vector<Off>& full,
+                const std::vector<std::vector<int>>& members,
+                const std::vector<std::array<qf, 3>>& pts,
+                const std::vector<std::array<int, 3>>& alphas, std::vector<qf>& faceq,
+                std::vector<qf>& derivq) {
+  struct Elem {
+    int perm[3], sgn[3];
+  };
+  std::vector<Elem> G;
+  int p[3] = {0, 1, 2};
+  do {
+    if (dim == 2 && p[2] != 2) continue;
+    for (int m = 0; m < (1 << dim); ++m) {
+      Elem e{};
+      for (int b = 0; b < 3; ++b) {
+        e.perm[b] = p[b];
+        e.sgn[b] = (b < dim && ((m >> b) & 1)) ? -1 : 1;
+      }
+      G.push_back(e);
+    }
+  } while (std::next_permutation(p, p + 3));
+  const int NF = t.n_full, NS = t.n_stencils, NP = t.n_points, NA = t.n_alpha;
+  auto apply = [&](const Elem& g, const Off& o) {
+    Off r{{0, 0, 0}};
+    for (int b = 0; b < 3; ++b) r.c[b] = g.sgn[b] * o.c[g.perm[b]];
+    return r;
+  };
+  auto full_index = [&](const Off& o) {
+    for (int h = 0; h < NF; ++h)
+      if (full[h].c[0] == o.c[0] && full[h].c[1] == o.c[1] && full[h].c[2] == o.c[2]) return h;
+    throw std::runtime_error("symmetry maps a stencil cell outside S0");
+  };
+  // per element: full-stencil cell map, stencil map, local position maps,
+  // point map, derivative map and sign
+  const int nG = (int)G.size();
+  std::vector<int> cmap((size_t)nG * NF), qmap((size_t)nG * NS), smap((size_t)nG * NP),
+      amap((size_t)nG * NA), asgn((size_t)nG * NA);
+  std::vector<std::vector<int>> local(NS, std::vector<int>(NF, -1));  // S0 index -> position in S_q
+  for (int q = 0; q < NS; ++q)
+    for (int l = 0; l < (int)members[q].size(); ++l) local[q][members[q][l]] = l;
+  for (int gi = 0; gi < nG; ++gi) {
+    const Elem& g = G[gi];
+    for (int h = 0; h < NF; ++h) cmap[(size_t)gi * NF + h] = full_index(apply(g, full[h]));
+    for (int q = 0; q < NS; ++q) {
+      std::vector<int> img;
+      for (int h : members[q]) img.push_back(cmap[(size_t)gi * NF + h]);
+      std::sort(img.begin(), img.end());
+      int found = -1;
+      for (int q2 = 0; q2 < NS && found < 0; ++q2) {
+        std::vector<int> m2 = members[q2];
+        std::sort(m2.begin(), m2.end());
+        if (m2 == img) found = q2;
+      }
+      if (found < 0) throw std::runtime_error("symmetry does not map substencils onto substencils");
+      qmap[(size_t)gi * NS + q] = found;
+    }
+    for (int s = 0; s < NP; ++s) {
+      std::array<qf, 3> x{0, 0, 0};
+      for (int b = 0; b < 3; ++b) x[b] = (qf)g.sgn[b] * pts[s][g.perm[b]];
+      int found = -1;
+      for (int s2 = 0; s2 < NP && found < 0; ++s2) {
+        bool eq = true;
+        for (int b = 0; b < 3; ++b) eq = eq && fabsq(pts[s2][b] - x[b]) < 1e-30Q;
+        if (eq) found = s2;
+      }
+      if (found < 0) throw std::runtime_error("symmetry does not map face points onto face points");
+      smap[(size_t)gi * NP + s] = found;
+    }
+    for (int a = 0; a < NA; ++a) {
+      std::array<int, 3> al2{0, 0, 0};
+      int sg = 1;
+      for (int b = 0; b < 3; ++b) {
+        al2[b] = alphas[a][g.perm[b]];
+        if (g.sgn[b] < 0 && (al2[b] & 1)) sg = -sg;
+      }
+      int found = -1;
+      for (int a2 = 0; a2 < NA && found < 0; ++a2)
+        if (alphas[a2] == al2) found = a2;
+      if (found < 0) throw std::runtime_error("symmetry does not map derivative indices");
+      amap[(size_t)gi * NA + a] = found;
+      asgn[(size_t)gi * NA + a] = sg;
+    }
+  }
+  // orbit averages: rows of kind 0 (face points) and 1 (derivatives)
+  for (int kind = 0; kind < 2; ++kind) {
+    const int nr = kind ? NA : NP;
+    std::vector<qf>& val = kind ? derivq : faceq;
+    std::vector<char> done(val.size(), 0);
+    auto at = [&](int q, int r, int l) {
+      return (size_t)t.cell_offset[q] * nr + (size_t)r * t.size[q] + l;
+    };
+    for (int q = 0; q < NS; ++q)
+      for (int r = 0; r < nr; ++r)
+        for (int l = 0; l < t.size[q]; ++l) {
+          if (done[at(q, r, l)]) continue;
+          const int h = members[q][l];
+          qf sum = 0;
+          std::vector<std::pair<size_t, int>> img(nG);
+          for (int gi = 0; gi < nG; ++gi) {
+            const int q2 = qmap[(size_t)gi * NS + q];
+            const int r2 = kind ? amap[(size_t)gi * NA + r] : smap[(size_t)gi * NP + r];
+            const int sg = kind ? asgn[(size_t)gi * NA + r] : 1;
+            const int l2 = local[q2][cmap[(size_t)gi * NF + h]];
+            img[gi] = {at(q2, r2, l2), sg};
+            sum += (qf)sg * val[img[gi].first];
+          }
+          // an entry its own stabiliser maps to minus itself is exactly 0
+          bool odd = false;
+          for (int gi = 0; gi < nG; ++gi) odd = odd || (img[gi].first == img[0].first && img[gi].second != img[0].second);
+          const qf avg = odd ? (qf)0 : sum / (qf)nG;
+          for (const auto& [e, sg] : img) {
+            val[e] = (qf)sg * avg;
+            done[e] = 1;
+          }
+        }
+  }
+}
+
 struct TableStore {
   kfvm_table t;
   std::vector<int> offsets, gather, alpha;
@@ -369,6 +500,8 @@ kfvm_table* build_table(int dim, int R, double ell_over_delta) {
 
   st->face.assign((size_t)t.total_cells * t.n_points, 0.0);
   st->deriv.assign((size_t)t.total_cells * t.n_alpha, 0.0);
+  // binary128 solutions; rounded to FP64 after the orbit symmetrisation
+  std::vector<qf> faceq((size_t)t.total_cells * t.n_points, 0), derivq((size_t)t.total_cells * t.n_alpha, 0);
 
   for (int q = 0; q < t.n_stencils; ++q) {
     std::vector<Off> cells;
@@ -412,8 +545,8 @@ kfvm_table* build_table(int dim, int R, double ell_over_delta) {
       }
       const qf res = solve_refined(M, f, rhs, z);
       if (!(res < 1e-9Q)) throw std::runtime_error("block solve residual > 1e-9");
-      double* dst = st->face.data() + (size_t)t.cell_offset[q] * t.n_points + (size_t)s * N;
-      for (int l = 0; l < N; ++l) dst[l] = (double)z[l];
+      qf* dst = faceq.data() + (size_t)t.cell_offset[q] * t.n_points + (size_t)s * N;
+      for (int l = 0; l < N; ++l) dst[l] = z[l];
     }
     // derivative vectors at the cell centre (kernel_recon.hpp:49-54)
     for (int ia = 0; ia < t.n_alpha; ++ia) {
@@ -434,10 +567,14 @@ kfvm_table* build_table(int dim, int R, double ell_over_delta) {
       }
       const qf res = solve_refined(M, f, rhs, z);
       if (!(res < 1e-9Q)) throw std::runtime_error("block solve residual > 1e-9");
-      double* dst = st->deriv.data() + (size_t)t.cell_offset[q] * t.n_alpha + (size_t)ia * N;
-      for (int l = 0; l < N; ++l) dst[l] = (double)z[l];
+      qf* dst = derivq.data() + (size_t)t.cell_offset[q] * t.n_alpha + (size_t)ia * N;
+      for (int l = 0; l < N; ++l) dst[l] = z[l];
     }
   }
+
+  symmetrize(dim, t, full, members, pts, alphas, faceq, derivq);
+  for (size_t i = 0; i < faceq.size(); ++i) st->face[i] = (double)faceq[i];
+  for (size_t i = 0; i < derivq.size(); ++i) st->deriv[i] = (double)derivq[i];
 
   // WENO-AO linear weights (§3.2), evaluated in FP64 in
   // the order written there.

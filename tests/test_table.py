@@ -128,32 +128,50 @@ def test_linear_weights(rset):
     assert g.tolist() == pytest.approx(ref, rel=1e-14)
 
 
-def test_mirror_symmetry_x(rset):
-    """the vector of a mirrored quadrature point on a mirror-symmetric
-    stencil equals the permuted original.  x -> -x maps W<->E faces and the
-    +x/-x biased substencils onto each other."""
-    dim, R = rset.dim, rset.R
-    rp = rset.n_face_points() // (2 * dim)
+def _group(dim):
+    """Signed axis permutations g(x)_b = s_b x_pi(b) of the square / cube."""
+    import itertools
+    for perm in itertools.permutations(range(dim)):
+        for signs in itertools.product((1, -1), repeat=dim):
+            yield tuple(perm) + tuple(range(dim, 3)), tuple(signs) + (1,) * (3 - dim)
+
+
+def test_exact_symmetry_every_group_element(rset):
+    """kernel_recon.hpp:105-106 / S:223: the vector of a mirrored or rotated
+    quadrature point (derivative) on the image (sub)stencil is EXACTLY the
+    permuted original (derivatives: times the sign of the odd flipped orders),
+    for every element of the square's / cube's symmetry group (x, y, z mirrors
+    and axis swaps) — tolerance 0."""
+    dim = rset.dim
     pos = {tuple(o): h for h, o in enumerate(rset.offsets)}
-
-    def mirror_q(q):
-        return {2: 3, 3: 2}.get(q, q)
-
-    def mirror_s(s):
-        f, m = divmod(s, rp)
-        if f in (0, 1):
-            return (1 - f) * rp + m
-        return s  # the other faces: x -> -x flips their first tangential node
-    worst = 0.0
-    for q in range(rset.n_stencils):
-        qm = mirror_q(q)
-        a, b = rset.st[q], rset.st[qm]
-        idx_b = {g: i for i, g in enumerate(b.gather)}
-        perm = [idx_b[pos[(-rset.offsets[g][0], rset.offsets[g][1], rset.offsets[g][2])]] for g in a.gather]
-        for s in range(rp * 2):  # W and E faces
-            worst = max(worst, np.abs(a.face[s] - b.face[mirror_s(s)][perm]).max())
-    tol = 0.0 if (dim, R) in ((2, 2), (3, 2)) else 1e-14
-    assert worst <= tol
+    members = [sorted(st.gather.tolist()) for st in rset.st]
+    pts = rset.points
+    n_el = 0
+    for perm, sg in _group(dim):
+        n_el += 1
+        gcell = {h: pos[tuple(sg[b] * rset.offsets[h][perm[b]] for b in range(3))]
+                 for h in range(len(rset.offsets))}
+        for q, st in enumerate(rset.st):
+            img = sorted(gcell[h] for h in st.gather)
+            q2 = members.index(img)
+            st2 = rset.st[q2]
+            loc2 = {h: i for i, h in enumerate(st2.gather)}
+            perm_l = [loc2[gcell[h]] for h in st.gather]
+            for s in range(len(pts)):
+                x2 = [sg[b] * pts[s][perm[b]] for b in range(3)]
+                s2 = int(np.argmin(np.abs(pts - x2).sum(1)))
+                assert np.abs(pts[s2] - x2).max() < 1e-15
+                out = np.empty(st2.count)
+                out[perm_l] = st.face[s]
+                assert np.array_equal(out, st2.face[s2]), (perm, sg, q, s)
+            al = [tuple(a) for a in rset.alphas]
+            for a, alpha in enumerate(al):
+                a2 = tuple(alpha[perm[b]] for b in range(3))
+                sign = np.prod([sg[b] for b in range(3) if a2[b] % 2])
+                out = np.empty(st2.count)
+                out[perm_l] = sign * st.deriv[a]
+                assert np.array_equal(out, st2.deriv[al.index(a2)]), (perm, sg, q, alpha)
+    assert n_el == (8 if dim == 2 else 48)
 
 
 def test_golden_mpmath_vectors():
