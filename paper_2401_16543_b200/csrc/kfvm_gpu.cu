@@ -148,6 +148,7 @@ constexpr int npoints(int dim, int R) { return dim == 2 ? 4 * R : 6 * R * R; }
 #include "kfvm_recon.cuh"
 #include "kfvm_recon_u.cuh"
 #include "kfvm_recon_row.cuh"
+#include "kfvm_fused3.cuh"
 
 // ------------------------------------------------------------------ k_flux
 template <int DIM>
@@ -711,12 +712,18 @@ struct kfvm_handle {
   cudaGraphExec_t graph = nullptr;
   bool timing = false;
   bool fast = true;
-  int engine = 2;  // 0 generic (k_states), 1 unrolled DFMA (k_states_fast), 2 tensor core (k_states_u)
+  // 0 generic (k_states), 1 unrolled DFMA (k_states_fast), 2 tensor core (k_states_u),
+  // 3 fused 2-D stage, 4 row-marching DFMA (2-D), 5 fused 3-D stage (k_fused3)
+  int engine = 2;
   int kz = 16;     // planes marched by one k_states_u CTA
   bool visc = false;  // Navier-Stokes fluxes (k_visc after the face fluxes)
   bool grav = false;  // gravity source in k_update
   double *d_Bd = nullptr, *d_Bf = nullptr;
   int* d_gat4 = nullptr;
+  int* d_gat8 = nullptr;    // chunk tables of the fused 3-D engine's 8x4 tile
+  double* d_edges = nullptr;  // tile-edge face states of the fused 3-D engine
+  size_t edge_elems = 0;
+  Edges eds{};
   cudaEvent_t ev[2];
   double t_states = 0, t_flux = 0, t_update = 0, t_other = 0;
   nccl_comm comm = nullptr;
@@ -946,9 +953,65 @@ void launch_flux(kfvm_handle* h, const Chunk& ch) {
   toc(h, &h->t_flux);
 }
 
+// the fused 3-D stage engine (k_fused3 + k_edges3): no face-state scratch
+bool fused3(const kfvm_handle* h) { return h->dim == 3 && h->R == 2 && h->engine == 5 && !h->kx; }
+
+// z-block layout of the stage's fused launches: disjoint plane ranges of the
+// extended box, sorted by their first plane
+void set_ranges(kfvm_handle* h, int n, const int* r0, const int* r1) {
+  Edges& E = h->eds;
+  E.nr = n;
+  for (int i = 0; i < n; ++i) {
+    E.r0[i] = r0[i];
+    E.r1[i] = r1[i];
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j)
+      if (E.r0[j] < E.r0[i]) {
+        std::swap(E.r0[i], E.r0[j]);
+        std::swap(E.r1[i], E.r1[j]);
+      }
+  int nb = 0;
+  for (int i = 0; i < n; ++i) nb += edge_nblocks(E, i);
+  E.nzs = nb - 1;
+}
+
+void launch_fused3(kfvm_handle* h, const double* U, const Chunk& ch) {
+  tic(h);
+  int rr = -1;
+  for (int i = 0; i < h->eds.nr; ++i)
+    if (h->eds.r0[i] == ch.e0 && h->eds.r1[i] == ch.e1) rr = i;
+  if (rr < 0) {  // a plane range outside the stage's layout: a programming error
+    fprintf(stderr, "kfvm: fused 3-D launch over an unregistered plane range\n");
+    abort();
+  }
+  const long long ntx = (ch.ex + kTX - 1) / kTX, nty = (ch.em + kTY - 1) / kTY;
+  const long long nb = ntx * nty * edge_nblocks(h->eds, rr);
+  k_fused3<2><<<(unsigned)nb, 128, FCfg<2>::bytes(), h->stream>>>(
+      U, h->Pr, h->F, h->g, ch, h->eds, rr, h->d_err, h->d_Bd, h->d_Bf, h->d_gat8);
+  dbg_sync(h, "k_fused3");
+  h->launches++;
+  toc(h, &h->t_states);
+}
+
+void launch_edges3(kfvm_handle* h, const Chunk& ch) {
+  tic(h);
+  const Edges& E = h->eds;
+  const long long n = (long long)E.nxe * ch.em * ch.ep + (long long)E.nye * ch.ex * ch.ep +
+                      (long long)E.nzs * ch.em * ch.ex;
+  k_edges3<2><<<blocks(n, 128), 128, 0, h->stream>>>(h->F, ch, E);
+  dbg_sync(h, "k_edges3");
+  h->launches++;
+  toc(h, &h->t_flux);
+}
+
 // states of the chunk's extended planes [ch.e0, ch.e1) (the fused 2-D
 // engine also produces the face fluxes)
 void states_only(kfvm_handle* h, const double* U, const Chunk& ch) {
+  if (fused3(h)) {
+    launch_fused3(h, U, ch);
+    return;
+  }
   if (h->dim == 2 && h->R == 2) launch_states<2, 2>(h, U, ch);
   if (h->dim == 2 && h->R == 3) launch_states<2, 3>(h, U, ch);
   if (h->dim == 3 && h->R == 2) launch_states<3, 2>(h, U, ch);
@@ -956,9 +1019,10 @@ void states_only(kfvm_handle* h, const double* U, const Chunk& ch) {
 }
 
 bool fused_engine(const kfvm_handle* h) { return h->dim == 2 && h->engine == 3 && !h->kx; }
-
 void flux_only(kfvm_handle* h, const Chunk& ch) {
-  if (!fused_engine(h)) {
+  if (fused3(h)) {
+    launch_edges3(h, ch);
+  } else if (!fused_engine(h)) {
     if (h->dim == 2 && h->R == 2) launch_flux<2, 2>(h, ch);
     if (h->dim == 2 && h->R == 3) launch_flux<2, 3>(h, ch);
     if (h->dim == 3 && h->R == 2) launch_flux<3, 2>(h, ch);
@@ -1167,6 +1231,10 @@ int run_stage(kfvm_handle* h, const double* Uin, double* Uout, int stage) {
     int rc = halo(h, const_cast<double*>(Uin), h->stream);
     if (rc) return rc;
     prims(h, Uin);
+    if (fused3(h)) {
+      const int r0 = 0, r1 = np + 2;
+      set_ranges(h, 1, &r0, &r1);
+    }
     run_planes(h, Uin, Uout, stage, 0, np);
     return KFVM_OK;
   }
@@ -1179,6 +1247,10 @@ int run_stage(kfvm_handle* h, const double* Uin, double* Uout, int stage) {
   prims(h, Uin, 0, np);
   if (nch == 1) {
     Chunk ch = make_chunk(h, 0, np);
+    if (fused3(h)) {
+      const int r0[3] = {R + 1, 0, np - R + 1}, r1[3] = {np - R + 1, R + 1, ch.ep};
+      set_ranges(h, 3, r0, r1);
+    }
     ch.e0 = R + 1;
     ch.e1 = np - R + 1;
     states_only(h, Uin, ch);
@@ -1427,6 +1499,70 @@ int ensure_aos(kfvm_handle* h) {
   return KFVM_OK;
 }
 
+// Scratch of the current engine.  The fused 3-D engine keeps no face states:
+// it needs the whole slab's face fluxes and the compact tile-edge buffers (one
+// chunk).  The other engines get a chunked face-state + flux scratch within
+// the budget: half the device memory still free after the state buffers (at
+// least st_budget = 16 GB when that much is free), or `chunk_planes` planes
+// when given (each chunk recomputes its two edge planes).
+int configure_scratch(kfvm_handle* h, long long chunk_planes) {
+  drop_graphs(h);
+  for (double** p : {&h->St, &h->F, &h->d_edges})
+    if (*p) {
+      cudaFree(*p);
+      *p = nullptr;
+    }
+  h->st_elems = h->f_elems = h->edge_elems = 0;
+  const int np = h->g.np_loc;
+  if (fused3(h)) {
+    h->chunk = np;
+    const Chunk ch = make_chunk(h, 0, np);
+    Edges& E = h->eds;
+    E.KZ = h->kz;
+    E.nxe = (ch.ex + kTX - 1) / kTX - 1;
+    E.nye = (ch.em + kTY - 1) / kTY - 1;
+    const int nzcap = (ch.ep + E.KZ - 1) / E.KZ + 3;  // the overlapped split adds <= 2 starts
+    E.sx = (long long)E.nxe * ch.em * ch.ep;
+    E.sy = (long long)E.nye * ch.ex * ch.ep;
+    E.sz = (long long)nzcap * ch.em * ch.ex;
+    const long long rows = 2LL * h->R * h->R * h->nv;  // [side][m][v]
+    h->edge_elems = (size_t)(rows * (E.sx + E.sy + E.sz));
+    h->f_elems = (size_t)ch.nfb * h->dim * h->nv;
+    CK(cudaMalloc(&h->F, h->f_elems * sizeof(double)));
+    CK(cudaMalloc(&h->d_edges, h->edge_elems * sizeof(double)));
+    E.x = h->d_edges;
+    E.y = E.x + rows * E.sx;
+    E.z = E.y + rows * E.sy;
+    const int r0 = 0, r1 = ch.ep;
+    set_ranges(h, 1, &r0, &r1);
+    return KFVM_OK;
+  }
+  const long long per_plane =
+      ((long long)(h->g.nx + 2) * (h->dim == 3 ? h->g.nm + 2 : 1) * h->NP +
+       (long long)(h->g.nx + 1) * (h->dim == 3 ? h->g.nm + 1 : 1) * h->dim) *
+      h->nv * (long long)sizeof(double);
+  long long c = chunk_planes;
+  if (c <= 0) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    long long budget = (long long)(0.5 * (double)fr);
+    if (budget < h->st_budget) budget = std::min(h->st_budget, (long long)(0.8 * (double)fr));
+    c = budget / per_plane - 2;
+  }
+  c = std::max(1LL, std::min(c, (long long)np));
+  if (h->kx && c < np)  // the flags of a chunk's edge planes need the pass-1 states beyond them
+    return fail(h, KFVM_ERR_CONFIG,
+                "kxrcf: the slab's face states must fit one chunk (scratch budget: half the "
+                "free device memory)");
+  h->chunk = (int)c;
+  const Chunk ch = make_chunk(h, 0, h->chunk);
+  h->st_elems = (size_t)ch.next * h->NP * h->nv;
+  h->f_elems = (size_t)ch.nfb * h->dim * h->nv;
+  CK(cudaMalloc(&h->St, h->st_elems * sizeof(double)));
+  CK(cudaMalloc(&h->F, h->f_elems * sizeof(double)));
+  return KFVM_OK;
+}
+
 // Upload the weights into the generated __constant__ arrays after checking
 // that the table's geometry is the structure compiled into kfvm_gen.cuh
 // (once per device: the registry's first handle).
@@ -1499,6 +1635,26 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
         }
       }
     }
+  }
+  if constexpr (D == 3) {
+    // the fused 3-D engine's region geometry (8 x 4 tile): same chunks and slots
+    std::vector<int> g8(g4);
+    constexpr int RX8 = kTX + 2 * R;
+    for (int q = 0, ck = 0; q < G::NS; ++q) {
+      const int N = t->size[q], o = t->cell_offset[q];
+      const int kcq = (N + 3) / 4, pad = 4 * kcq - N;
+      for (int jj = 0; jj < kcq; ++jj, ++ck)
+        for (int k = 0; k < 4; ++k) {
+          const int hh = 4 * jj + k - pad;
+          const int e = t->gather[o + (hh < 0 ? 0 : hh)];
+          g8[(size_t)(ck * 4 + k) * 2] = (G::OFF[e][1] + R) * RX8 + G::OFF[e][0] + R;
+        }
+    }
+    CK(cudaMalloc(&h->d_gat8, g8.size() * sizeof(int)));
+    CK(cudaMemcpy(h->d_gat8, g8.data(), g8.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if constexpr (R == 2)
+      CK(cudaFuncSetAttribute(k_fused3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)FCfg<2>::bytes()));
   }
   CK(cudaMalloc(&h->d_Bd, bd.size() * sizeof(double)));
   CK(cudaMalloc(&h->d_Bf, bf.size() * sizeof(double)));
@@ -1597,7 +1753,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   h->nv = cfg->dim + 2;
   h->NP = t->n_points;
   // measured: row-marching DFMA for 2-D, tensor cores for 3-D
-  h->engine = cfg->dim == 2 ? 4 : 2;
+  h->engine = cfg->dim == 2 ? 4 : (cfg->radius == 2 && !cfg->kxrcf ? 5 : 2);
   h->kz = cfg->dim == 2 ? 8 : 32;  // 3-D R=2: 32 measured 0.4 % faster than 16 (configs 3, 4)
   if (dist) {
     h->rank = dist->rank;
@@ -1781,40 +1937,11 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     bad(cudaMemset(h->Ua, 0, ufull * sizeof(double)), "memset");
     bad(cudaMemset(h->Ub, 0, ufull * sizeof(double)), "memset");
   }
-  // chunk planes so the face-state and flux scratch stay within budget: half
-  // the device memory still free after the state buffers (at least
-  // st_budget = 16 GB when that much is free), so large 3-D slabs run in few
-  // chunks (each chunk recomputes its two edge planes)
-  {
-    const long long per_plane =
-        ((long long)(h->g.nx + 2) * (h->dim == 3 ? h->g.nm + 2 : 1) * h->NP +
-         (long long)(h->g.nx + 1) * (h->dim == 3 ? h->g.nm + 1 : 1) * h->dim) *
-        h->nv * (long long)sizeof(double);
-    size_t fr = 0, tot = 0;
-    if (rc == KFVM_OK) cudaMemGetInfo(&fr, &tot);
-    long long budget = (long long)(0.5 * (double)fr);
-    if (budget < h->st_budget) budget = std::min(h->st_budget, (long long)(0.8 * (double)fr));
-    long long c = budget / per_plane - 2;
-    c = std::max(1LL, std::min(c, (long long)np));
-    h->chunk = (int)c;
-    if (h->kx && h->chunk < np) {
-      // the flags of a chunk's edge planes need the pass-1 states beyond them
-      rc = KFVM_ERR_CONFIG;
-      h->err = "kxrcf: the slab's face states must fit one chunk (scratch budget: half the "
-               "free device memory)";
-    }
-  }
+  if (rc == KFVM_OK) rc = configure_scratch(h, 0);
   if (h->kx && rc == KFVM_OK) {
     const Chunk ch = make_chunk(h, 0, h->chunk);
     bad(cudaMalloc(&h->d_flags, (size_t)ch.next), "cudaMalloc flags");
     if (rc == KFVM_OK) bad(cudaMemset(h->d_flags, 0, (size_t)ch.next), "memset flags");
-  }
-  {
-    const Chunk ch = make_chunk(h, 0, h->chunk);
-    h->st_elems = (size_t)ch.next * h->NP * h->nv;
-    h->f_elems = (size_t)ch.nfb * h->dim * h->nv;
-    bad(cudaMalloc(&h->St, h->st_elems * sizeof(double)), "cudaMalloc states");
-    bad(cudaMalloc(&h->F, h->f_elems * sizeof(double)), "cudaMalloc flux");
   }
   if (h->integrator == KFVM_SSP43 && rc == KFVM_OK) {
     const int nrow = h->dim == 3 ? h->g.nm : 1;
@@ -1904,7 +2031,7 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
   for (void* p : {(void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
                   (void*)h->aos, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
-                  (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_tt,
+                  (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_gat8, (void*)h->d_edges, (void*)h->d_tt,
                   (void*)h->d_flags, (void*)h->Uh, (void*)h->d_rows, (void*)h->d_planes,
                   (void*)h->d_ctl, (void*)h->d_nps, (void*)h->ext})
     if (p) cudaFree(p);
@@ -2024,6 +2151,18 @@ extern "C" int kfvm_gpu_states(kfvm_handle* h, double* states_host) {
     if (h->dim == 3 && h->R == 3) rc = kx_flags<3, 3>(h, h->U0, ch);
     if (rc) return rc;
   }
+  // the fused 3-D engine keeps no face states: this call runs the tensor-core
+  // states engine (same bits) over a temporary chunked scratch
+  const int eng_saved = h->engine;
+  const bool tmp_scratch = fused3(h);
+  if (tmp_scratch) {
+    h->engine = 2;
+    if ((rc = configure_scratch(h, 0))) {
+      h->engine = eng_saved;
+      configure_scratch(h, 0);
+      return rc;
+    }
+  }
   const size_t nbuf = (size_t)plane_cells * h->chunk * per_cell;
   if (h->ext_elems < nbuf) {
     if (h->ext) cudaFree(h->ext);
@@ -2045,7 +2184,13 @@ extern "C" int kfvm_gpu_states(kfvm_handle* h, double* states_host) {
                        cudaMemcpyDeviceToHost, h->stream));
   }
   CK(cudaStreamSynchronize(h->stream));
-  return check_err(h);
+  rc = check_err(h);
+  if (tmp_scratch) {
+    h->engine = eng_saved;
+    const int rc2 = configure_scratch(h, 0);
+    if (!rc) rc = rc2;
+  }
+  return rc;
 }
 
 // KXRCF flags (1 = WENO) of the rank's cells for the current state, AoS order
@@ -2300,16 +2445,16 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
   std::string n(name ? name : "");
   if (n == "fast_states" || n == "engine") {
     if (n == "engine") {
-      if (value < 0 || value > 4 || (value >= 3 && h->dim != 2))
+      if (value < 0 || value > 5 || ((value == 3 || value == 4) && h->dim != 2) ||
+          (value == 5 && !(h->dim == 3 && h->R == 2)))
         return fail(h, KFVM_ERR_CONFIG,
                     "engine: 0 generic, 1 DFMA, 2 tensor core, 3 fused 2-D stage, "
-                    "4 row-marching DFMA (2-D)");
+                    "4 row-marching DFMA (2-D), 5 fused 3-D stage (3-D R=2)");
       h->engine = (int)value;
     } else {
       h->engine = value ? 2 : 0;
     }
-    drop_graphs(h);
-    return KFVM_OK;
+    return configure_scratch(h, 0);
   }
   if (n == "ring_split") {
     drop_graphs(h);
@@ -2325,7 +2470,7 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
     if (value < 1) return fail(h, KFVM_ERR_CONFIG, "kz must be >= 1");
     h->kz = (int)value;
     drop_graphs(h);
-    return KFVM_OK;
+    return fused3(h) ? configure_scratch(h, 0) : KFVM_OK;
   }
   if (n == "timing") {
     h->timing = value != 0;
@@ -2333,28 +2478,19 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
     return KFVM_OK;
   }
   if (n == "chunk_planes" || n == "scratch_bytes") {
+    // chunking applies to the face-state engines; the fused 3-D engine has no
+    // face-state scratch and always runs the slab as one chunk
     long long c;
     if (n == "chunk_planes") {
       c = value;
     } else {
       const long long per_plane = (long long)(h->g.nx + 2) * (h->dim == 3 ? h->g.nm + 2 : 1) *
                                   h->NP * h->nv * (long long)sizeof(double);
-      c = value / per_plane - 2;
+      c = std::max(1LL, value / per_plane - 2);
     }
-    c = std::max(1LL, std::min(c, (long long)h->g.np_loc));
-    if (h->kx && c < h->g.np_loc)  // the KXRCF passes run on one chunk (checked at create too)
+    if (h->kx && std::min(c, (long long)h->g.np_loc) < h->g.np_loc)
       return fail(h, KFVM_ERR_CONFIG, "kxrcf: the slab's face states must fit one chunk");
-    drop_graphs(h);
-    cudaFree(h->St);
-    cudaFree(h->F);
-    h->St = h->F = nullptr;
-    h->chunk = (int)c;
-    const Chunk ch = make_chunk(h, 0, h->chunk);
-    h->st_elems = (size_t)ch.next * h->NP * h->nv;
-    h->f_elems = (size_t)ch.nfb * h->dim * h->nv;
-    CK(cudaMalloc(&h->St, h->st_elems * sizeof(double)));
-    CK(cudaMalloc(&h->F, h->f_elems * sizeof(double)));
-    return KFVM_OK;
+    return configure_scratch(h, c);
   }
   return fail(h, KFVM_ERR_CONFIG, "unknown option " + n);
 }

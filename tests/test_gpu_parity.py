@@ -95,6 +95,7 @@ def test_chunked_equals_unchunked(require_gpu):
         d1 = s.advance(2)
         A = s.get_state()
     with K.Solver(g, rset) as s:
+        s.set_option("engine", 2)  # the face-state engines run in chunks
         s.set_option("chunk_planes", 5)
         s.set_state(U)
         d2 = s.advance(2)
@@ -133,11 +134,12 @@ def test_runtime_error_on_inadmissible_state(require_gpu):
 
 @pytest.mark.parametrize("idx,n", [(1, 20), (2, 24), (3, 10), (4, 10), (5, 10)])
 def test_engines_bitwise_identical(require_gpu, idx, n):
-    """generic / unrolled-DFMA / DMMA / row-marching DFMA reconstruction engines agree
-    bit for bit."""
+    """generic / unrolled-DFMA / DMMA / row-marching DFMA reconstruction engines and
+    the fused 3-D stage engine agree bit for bit."""
     g, ic, U, rset = _setup(idx, n, {})
     outs = []
-    for eng in ((0, 1, 2, 3, 4) if g.dim == 2 else (0, 1, 2)):
+    engines = (0, 1, 2, 3, 4) if g.dim == 2 else ((0, 1, 2, 5) if g.radius == 2 else (0, 1, 2))
+    for eng in engines:
         with K.Solver(g, rset) as s:
             s.set_option("engine", eng)
             s.set_state(U)
