@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(128, 3)
   const int icr = (w + R) * C::RX + r8 + R;               // cell centre in a region plane
   const int icn = (w + 1) * C::NX + r8 + 1;               // cell centre in a prims plane
   const int qb = lane & ~3;
+  PHASE_T0();
   for (int c = cstart; c < cend; ++c) {
     const int p = ch.c0 - 1 + c;
     if (c + 1 < cend) {
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(128, 3)
       ke = fma(T.ut[2], T.ut[2], ke);
       T.ke = 0.5 * ke;
     }
+    PHASE_MARK(0);
     // ---- pass 1: derivative columns -> beta (k_states_u order)
     {
       constexpr int NDM = C::NDM, NT = C::NT, NTA = NT > 0 ? NT : 1;
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(128, 3)
       }
     }
     __syncwarp();
+    PHASE_MARK(1);
     // ---- nonlinear weights (k_states_u order)
 #pragma unroll
     for (int q = k4; q < NS; q += 4)
@@ -312,6 +315,7 @@ __global__ void __launch_bounds__(128, 3)
       for (int q = 1; q < NS; ++q) sCw[(q * nv + v) * 8 + r8] = fma(-c0, c_t.gamma_lin[q], wt[q] * inv_sum);
     }
     __syncwarp();
+    PHASE_MARK(2);
     // ---- pass 2: every face point, one chain per (variable, point) through all stencils
     double V[nv][NPT][2];
     {
@@ -360,6 +364,7 @@ __global__ void __launch_bounds__(128, 3)
         }
       }
     }
+    PHASE_MARK(3);
     // ---- Phi^-1 and the positivity limiter (the k_states_u epilogue)
     double st[NPT][2][nv];
 #pragma unroll
@@ -453,6 +458,7 @@ __global__ void __launch_bounds__(128, 3)
             for (int v = 0; v < nv; ++v) st[n][e][v] = fma(thp, st[n][e][v] - Ubar[v], Ubar[v]);
       }
     }
+    PHASE_MARK(4);
     // ---- face-state exchange.  Lane k4 holds face points m = 2 (k4 & 1) + e
     // of the minus (k4 < 2) or plus (k4 >= 2) faces.
     const bool plus = k4 >= 2;
@@ -488,6 +494,7 @@ __global__ void __launch_bounds__(128, 3)
       }
     }
     __syncthreads();  // N states of every tile row visible
+    PHASE_MARK(5);
     // ---- Riemann solves: lane k4 takes point m = k4 of the cell's W, S, B faces
     const bool inx = a >= 1 && a <= ch.ex - 2, iny = b >= 1 && b <= ch.em - 2,
                inz = c >= 1 && c <= ch.ep - 2;
@@ -561,8 +568,10 @@ __global__ void __launch_bounds__(128, 3)
 #pragma unroll
         for (int v = 0; v < nv; ++v) tb[(mb + e) * nv + v] = st[2][e][v];
     }
+    PHASE_MARK(6);
     __pipeline_wait_prior(0);
     __syncthreads();
+    PHASE_MARK(7);
   }
 }
 

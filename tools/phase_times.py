@@ -10,7 +10,7 @@ import paper_2401_16543_b200 as K  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 128
-eng = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+eng = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 w = K.baseline_config(cfg, n=n)
 L = K._lib()
 buf = (C.c_ulonglong * 8)()
@@ -21,7 +21,11 @@ with K.Solver(w.grid) as s:
     L.kfvm_phase_cycles(buf, 1)
     s.advance(2)
     L.kfvm_phase_cycles(buf, 0)
-names = ["plane-setup", "pass1", "omega", "pass2", "phiinv+limiter+store", "wait+sync", "-", "-"]
+if eng == 5:
+    names = ["plane-setup", "pass1", "omega", "pass2", "phiinv+limiter", "exchange+edges+sync",
+             "riemann+quadrature+F", "wait+sync"]
+else:
+    names = ["plane-setup", "pass1", "omega", "pass2", "phiinv+limiter+store", "wait+sync", "-", "-"]
 tot = sum(buf) or 1
-for i in range(6):
+for i in range(8):
     print(f"{names[i]:12s} {buf[i]:16d}  {100.0 * buf[i] / tot:5.1f}%")
