@@ -27,6 +27,9 @@
 #define KFVM_FUSED3_CUH_
 
 constexpr int kTX = 8, kTY = 4;  // tile: 8 x-cells x 4 rows, warp = row
+#ifndef KFVM_F3_MINB  // resident CTAs per SM the register budget is sized for
+#define KFVM_F3_MINB 3
+#endif
 
 template <int R>
 struct FCfg {
@@ -94,7 +97,7 @@ __device__ __forceinline__ void edge_store(double* buf, long long rowlen, int si
 }
 
 template <int R>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128, KFVM_F3_MINB)
     k_fused3(const double* __restrict__ U, const double* __restrict__ Pr, double* __restrict__ F,
              Geo g, Chunk ch, Edges E, int rng, int* __restrict__ err,
              const double* __restrict__ Bd, const double* __restrict__ Bf,
@@ -520,20 +523,25 @@ __global__ void __launch_bounds__(128, 3)
         const double x1v = __shfl_sync(0xffffffffu, st[0][1][v], srcL);
         UL[v] = odd ? x1v : x0v;
       }
+      // all three solves as straight-line code (interleaved for ILP); the
+      // left states of an invalid face are whatever the buffers hold and the
+      // result is discarded
+      double ULy[nv], ULz[nv];
+      const double* nb = sN + (((w > 0 ? w - 1 : 0) * kTX + r8) * RP + k4) * nv;
+      const double* tb = sT + ((w * kTX + r8) * RP + k4) * nv;
 #pragma unroll
-      for (int v = 0; v < nv; ++v) FL[0][v] = FL[1][v] = FL[2][v] = 0.0;
-      if (vx) d_riemann_dir<3, 0>(c_k, UL, UR[0], FL[0]);
-      if (vy) {
-        const double* nb = sN + (((w - 1) * kTX + r8) * RP + k4) * nv;
-#pragma unroll
-        for (int v = 0; v < nv; ++v) UL[v] = nb[v];
-        d_riemann_dir<3, 1>(c_k, UL, UR[1], FL[1]);
+      for (int v = 0; v < nv; ++v) {
+        ULy[v] = nb[v];
+        ULz[v] = tb[v];
       }
-      if (vz) {
-        const double* tb = sT + ((w * kTX + r8) * RP + k4) * nv;
+      d_riemann_sel<3, 0>(c_k, UL, UR[0], FL[0]);
+      d_riemann_sel<3, 1>(c_k, ULy, UR[1], FL[1]);
+      d_riemann_sel<3, 2>(c_k, ULz, UR[2], FL[2]);
 #pragma unroll
-        for (int v = 0; v < nv; ++v) UL[v] = tb[v];
-        d_riemann_dir<3, 2>(c_k, UL, UR[2], FL[2]);
+      for (int v = 0; v < nv; ++v) {
+        FL[0][v] = vx ? FL[0][v] : 0.0;
+        FL[1][v] = vy ? FL[1][v] : 0.0;
+        FL[2][v] = vz ? FL[2][v] : 0.0;
       }
     }
     // ---- face quadrature: lane d of the quad forms face d's flux in point order
