@@ -27,6 +27,10 @@
 #define KFVM_FUSED3_CUH_
 
 constexpr int kTX = 8, kTY = 4;  // tile: 8 x-cells x 4 rows, warp = row
+// KFVM_ABL_* (timing ablations for tools/gpu/r2_abl.sh; results are wrong
+// when any is set): NOPHI skips the stencil transforms in both passes,
+// NORIEMANN the Riemann solves, NOLIMIT the limiter, NOBETA the smoothness
+// indicators, NOTAIL the tail derivative chains.
 #ifndef KFVM_F3_MINB  // resident CTAs per SM the register budget is sized for
 #define KFVM_F3_MINB 3
 #endif
@@ -236,22 +240,39 @@ __global__ void __launch_bounds__(128, KFVM_F3_MINB)
         for (int t = 0; t < NT; ++t) btn[t] = Bd[(cn * ND + ND - 1) * 32 + 4 * t + k4];
         double aw[nv];
 #pragma unroll
-        for (int v = 0; v < nv; ++v) aw[v] = phi_row<3>(T, av, v);
+        for (int v = 0; v < nv; ++v) {
+#ifdef KFVM_ABL_NOPHI
+          aw[v] = av[v];
+#else
+          aw[v] = phi_row<3>(T, av, v);
+#endif
+        }
 #pragma unroll
         for (int n = 0; n < NDM; ++n)
 #pragma unroll
           for (int v = 0; v < nv; ++v) dmma(acc[v][n][0], acc[v][n][1], aw[v], bv[n]);
+#ifndef KFVM_ABL_NOTAIL
 #pragma unroll
         for (int t = 0; t < NT; ++t)
 #pragma unroll
           for (int v = 0; v < nv; ++v) tl[v][t] = fma(bt[t], aw[v], tl[v][t]);
+#endif
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
         for (int n = 0; n < NDM; ++n) bv[n] = bn[n];
 #pragma unroll
         for (int t = 0; t < NT; ++t) bt[t] = btn[t];
+#ifdef KFVM_ABL_NOBETA
+        if ((sQ[ck] & 256) && k4 == 0) {
+#pragma unroll
+          for (int v = 0; v < nv; ++v) sCw[(q * nv + v) * 8 + r8] = acc[v][0][0];
+          ++q;
+        }
+        if (false) {
+#else
         if (sQ[ck] & 256) {
+#endif
           double bq[nv];
 #pragma unroll
           for (int v = 0; v < nv; ++v) bq[v] = 0.0;
@@ -351,7 +372,13 @@ __global__ void __launch_bounds__(128, KFVM_F3_MINB)
         for (int n = 0; n < NPT; ++n) bn[n] = Bf[(cn * NPT + n) * 32 + lane];
         double aw[nv];
 #pragma unroll
-        for (int v = 0; v < nv; ++v) aw[v] = cq[v] * phi_row<3>(T, av, v);
+        for (int v = 0; v < nv; ++v) {
+#ifdef KFVM_ABL_NOPHI
+          aw[v] = cq[v] * av[v];
+#else
+          aw[v] = cq[v] * phi_row<3>(T, av, v);
+#endif
+        }
 #pragma unroll
         for (int n = 0; n < NPT; ++n)
 #pragma unroll
@@ -415,6 +442,7 @@ __global__ void __launch_bounds__(128, KFVM_F3_MINB)
 #pragma unroll
       for (int d = 0; d < 3; ++d) Ubar[1 + d] = T.mt[d];
       Ubar[nv - 1] = plane(R)[(nv - 1) * C::RROW + icr];
+#ifndef KFVM_ABL_NOLIMIT
       double th = 1.0;
 #pragma unroll
       for (int n = 0; n < NPT; ++n)
@@ -460,6 +488,7 @@ __global__ void __launch_bounds__(128, KFVM_F3_MINB)
 #pragma unroll
             for (int v = 0; v < nv; ++v) st[n][e][v] = fma(thp, st[n][e][v] - Ubar[v], Ubar[v]);
       }
+#endif
     }
     PHASE_MARK(4);
     // ---- face-state exchange.  Lane k4 holds face points m = 2 (k4 & 1) + e
@@ -534,9 +563,18 @@ __global__ void __launch_bounds__(128, KFVM_F3_MINB)
         ULy[v] = nb[v];
         ULz[v] = tb[v];
       }
+#ifdef KFVM_ABL_NORIEMANN
+#pragma unroll
+      for (int v = 0; v < nv; ++v) {
+        FL[0][v] = UL[v] + UR[0][v];
+        FL[1][v] = ULy[v] + UR[1][v];
+        FL[2][v] = ULz[v] + UR[2][v];
+      }
+#else
       d_riemann_sel<3, 0>(c_k, UL, UR[0], FL[0]);
       d_riemann_sel<3, 1>(c_k, ULy, UR[1], FL[1]);
       d_riemann_sel<3, 2>(c_k, ULz, UR[2], FL[2]);
+#endif
 #pragma unroll
       for (int v = 0; v < nv; ++v) {
         FL[0][v] = vx ? FL[0][v] : 0.0;
