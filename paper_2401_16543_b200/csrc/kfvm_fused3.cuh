@@ -202,19 +202,15 @@ __global__ void __launch_bounds__(128, KFVM_F3_MINB)
       T.ke = 0.5 * ke;
     }
     PHASE_MARK(0);
-    // ---- pass 1: derivative columns -> beta (k_states_u order)
+    // ---- pass 1: derivative columns -> beta (k_states_u order).  The stencil
+    // structure is unrolled at compile time and two accumulator sets
+    // alternate between stencils, so the smoothness indicator of stencil q
+    // (its partial sums, tail chains and quad reductions) is formed while the
+    // DMMAs of stencil q + 1 are in flight instead of stalling on them.
     {
       constexpr int NDM = C::NDM, NT = C::NT, NTA = NT > 0 ? NT : 1;
-      double acc[nv][NDM][2];
-      double tl[nv][NTA];
-#pragma unroll
-      for (int u = 0; u < nv; ++u) {
-#pragma unroll
-        for (int n = 0; n < NDM; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
-#pragma unroll
-        for (int t = 0; t < NTA; ++t) tl[u][t] = 0.0;
-      }
-      int q = 0;
+      double acc[2][nv][NDM][2];
+      double tl[2][nv][NTA];
       double av[nv], bv[NDM], bt[NTA];
       {
         const int inpl = sTab[2 * k4], oz = sTab[2 * k4 + 1];
@@ -226,93 +222,91 @@ __global__ void __launch_bounds__(128, KFVM_F3_MINB)
 #pragma unroll
         for (int t = 0; t < NT; ++t) bt[t] = Bd[(ND - 1) * 32 + 4 * t + k4];
       }
-#pragma unroll kUChunkUnroll
-      for (int ck = 0; ck < G::NCHUNK; ++ck) {
-        const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
-        const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
-        const double* ap = plane(oz + R) + inpl + cb;
-        double an[nv], bn[NDM], btn[NTA];
+      // beta of stencil q from accumulator set s (k_states_u's operation order)
+      auto beta = [&](int q, int s) {
+        double bq[nv];
 #pragma unroll
-        for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
-#pragma unroll
-        for (int n = 0; n < NDM; ++n) bn[n] = Bd[(cn * ND + n) * 32 + lane];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) btn[t] = Bd[(cn * ND + ND - 1) * 32 + 4 * t + k4];
-        double aw[nv];
-#pragma unroll
-        for (int v = 0; v < nv; ++v) {
-#ifdef KFVM_ABL_NOPHI
-          aw[v] = av[v];
-#else
-          aw[v] = phi_row<3>(T, av, v);
-#endif
-        }
+        for (int v = 0; v < nv; ++v) bq[v] = 0.0;
 #pragma unroll
         for (int n = 0; n < NDM; ++n)
 #pragma unroll
-          for (int v = 0; v < nv; ++v) dmma(acc[v][n][0], acc[v][n][1], aw[v], bv[n]);
-#ifndef KFVM_ABL_NOTAIL
+          for (int e = 0; e < 2; ++e) {
+            const int al = 8 * n + 2 * k4 + e;
+            const double sc = al < G::NA ? c_t.scale[al] : 0.0;
 #pragma unroll
-        for (int t = 0; t < NT; ++t)
+            for (int v = 0; v < nv; ++v)
+              if (al < G::NA) bq[v] = fma(sc, acc[s][v][n][e] * acc[s][v][n][e], bq[v]);
+          }
 #pragma unroll
-          for (int v = 0; v < nv; ++v) tl[v][t] = fma(bt[t], aw[v], tl[v][t]);
-#endif
+        for (int t = 0; t < NT; ++t) {
+          const int al = 8 * NDM + t;
 #pragma unroll
-        for (int u = 0; u < nv; ++u) av[u] = an[u];
-#pragma unroll
-        for (int n = 0; n < NDM; ++n) bv[n] = bn[n];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) bt[t] = btn[t];
-#ifdef KFVM_ABL_NOBETA
-        if ((sQ[ck] & 256) && k4 == 0) {
-#pragma unroll
-          for (int v = 0; v < nv; ++v) sCw[(q * nv + v) * 8 + r8] = acc[v][0][0];
-          ++q;
+          for (int v = 0; v < nv; ++v) {
+            double d = tl[s][v][t] + __shfl_xor_sync(0xffffffffu, tl[s][v][t], 1);
+            d = d + __shfl_xor_sync(0xffffffffu, d, 2);
+            if ((t >> 1) == k4) bq[v] = fma(c_t.scale[al], d * d, bq[v]);
+          }
         }
-        if (false) {
-#else
-        if (sQ[ck] & 256) {
-#endif
-          double bq[nv];
 #pragma unroll
-          for (int v = 0; v < nv; ++v) bq[v] = 0.0;
+        for (int v = 0; v < nv; ++v) {
+          bq[v] = bq[v] + __shfl_xor_sync(0xffffffffu, bq[v], 1);
+          bq[v] = bq[v] + __shfl_xor_sync(0xffffffffu, bq[v], 2);
+        }
+        if (k4 == 0) {
+#pragma unroll
+          for (int v = 0; v < nv; ++v) sCw[(q * nv + v) * 8 + r8] = bq[v];
+        }
+      };
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        const int s = q & 1;
+#pragma unroll
+        for (int u = 0; u < nv; ++u) {
+#pragma unroll
+          for (int n = 0; n < NDM; ++n) acc[s][u][n][0] = acc[s][u][n][1] = 0.0;
+#pragma unroll
+          for (int t = 0; t < NTA; ++t) tl[s][u][t] = 0.0;
+        }
+#pragma unroll
+        for (int jj = 0; jj < G::kc(q); ++jj) {
+          const int ck = G::cbase(q) + jj;
+          const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
+          const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
+          const double* ap = plane(oz + R) + inpl + cb;
+          double an[nv], bn[NDM], btn[NTA];
+#pragma unroll
+          for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
+#pragma unroll
+          for (int n = 0; n < NDM; ++n) bn[n] = Bd[(cn * ND + n) * 32 + lane];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) btn[t] = Bd[(cn * ND + ND - 1) * 32 + 4 * t + k4];
+          double aw[nv];
+#pragma unroll
+          for (int v = 0; v < nv; ++v) {
+#ifdef KFVM_ABL_NOPHI
+            aw[v] = av[v];
+#else
+            aw[v] = phi_row<3>(T, av, v);
+#endif
+          }
 #pragma unroll
           for (int n = 0; n < NDM; ++n)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int al = 8 * n + 2 * k4 + e;
-              const double sc = al < G::NA ? c_t.scale[al] : 0.0;
+            for (int v = 0; v < nv; ++v) dmma(acc[s][v][n][0], acc[s][v][n][1], aw[v], bv[n]);
 #pragma unroll
-              for (int v = 0; v < nv; ++v)
-                if (al < G::NA) bq[v] = fma(sc, acc[v][n][e] * acc[v][n][e], bq[v]);
-            }
+          for (int t = 0; t < NT; ++t)
 #pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            const int al = 8 * NDM + t;
+            for (int v = 0; v < nv; ++v) tl[s][v][t] = fma(bt[t], aw[v], tl[s][v][t]);
 #pragma unroll
-            for (int v = 0; v < nv; ++v) {
-              double d = tl[v][t] + __shfl_xor_sync(0xffffffffu, tl[v][t], 1);
-              d = d + __shfl_xor_sync(0xffffffffu, d, 2);
-              if ((t >> 1) == k4) bq[v] = fma(c_t.scale[al], d * d, bq[v]);
-              tl[v][t] = 0.0;
-            }
-          }
+          for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
-          for (int v = 0; v < nv; ++v) {
-            bq[v] = bq[v] + __shfl_xor_sync(0xffffffffu, bq[v], 1);
-            bq[v] = bq[v] + __shfl_xor_sync(0xffffffffu, bq[v], 2);
-          }
-          if (k4 == 0) {
+          for (int n = 0; n < NDM; ++n) bv[n] = bn[n];
 #pragma unroll
-            for (int v = 0; v < nv; ++v) sCw[(q * nv + v) * 8 + r8] = bq[v];
-          }
-#pragma unroll
-          for (int u = 0; u < nv; ++u)
-#pragma unroll
-            for (int n = 0; n < NDM; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
-          ++q;
+          for (int t = 0; t < NT; ++t) bt[t] = btn[t];
+          if (q > 0 && jj == 0) beta(q - 1, s ^ 1);  // after the first chunk of stencil q
         }
       }
+      beta(NS - 1, (NS - 1) & 1);
     }
     __syncwarp();
     PHASE_MARK(1);
