@@ -1752,8 +1752,13 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   h->R = cfg->radius;
   h->nv = cfg->dim + 2;
   h->NP = t->n_points;
-  // measured: row-marching DFMA for 2-D, tensor cores for 3-D
-  h->engine = cfg->dim == 2 ? 4 : (cfg->radius == 2 && !cfg->kxrcf ? 5 : 2);
+  // measured: row-marching DFMA for 2-D, tensor cores for 3-D.
+  // The fused 3-D stage engine (5) is bit-identical but slower on B200: config
+  // 3 132.3 vs 128.8 ms/step, config 4 1118.7 vs 1019.3 (profiles/r02) — the
+  // in-kernel Riemann solves run at the reconstruction kernel's 12 warps/SM
+  // instead of k_flux's full occupancy, and the face-state round trip they
+  // save is not the bound (the stage is FP64-datapath bound)
+  h->engine = cfg->dim == 2 ? 4 : 2;
   h->kz = cfg->dim == 2 ? 8 : 32;  // 3-D R=2: 32 measured 0.4 % faster than 16 (configs 3, 4)
   if (dist) {
     h->rank = dist->rank;

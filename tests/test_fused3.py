@@ -42,6 +42,7 @@ def test_fused3_run_bitwise(require_gpu, idx, shape, kz):
 def test_fused3_rhs_and_hll(require_gpu, idx):
     g, ic, U, rset = _case(idx, (12, 11, 10), riemann="hll")
     with K.Solver(g, rset) as s:
+        s.set_option("engine", 5)
         L = s.compute_rhs(U)
     assert np.array_equal(L, Oracle(g, rset).compute_rhs(U))
 
@@ -55,6 +56,7 @@ def test_fused3_overlapped_ranges(require_gpu, kz):
     outs = []
     for ov in (0, 1):
         with K.Solver(g, rset) as s:
+            s.set_option("engine", 5)
             s.set_option("kz", kz)
             s.set_option("overlap", ov)
             s.set_state(U)
