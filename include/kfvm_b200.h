@@ -207,6 +207,14 @@ typedef struct kfvm_dist {
 } kfvm_dist;
 
 int kfvm_nccl_unique_id(unsigned char id[128]);
+/* In-process loopback group id (no reference counterpart; test transport):
+ * pass it as kfvm_dist.nccl_id to nranks handles created in ONE process on
+ * the same device, each then driven by its own host thread like a rank.
+ * Halo planes, KXRCF edge flags, the dt maximum and the SSP(4,3) error
+ * planes are exchanged by device-to-device copies with NCCL's send/recv and
+ * collective semantics; loopback handles run their steps eagerly (the
+ * host-side rendezvous cannot be graph-captured). */
+int kfvm_loopback_id(unsigned char id[128]);
 
 /* Slab owned by `rank`: planes [*p0, *p0 + *np) of the slab axis. */
 void kfvm_slab_range(int n_global, int nranks, int rank, int* p0, int* np);

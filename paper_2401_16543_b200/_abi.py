@@ -72,6 +72,7 @@ EXPORTS = [
     ("kfvm_ic_generate", C.c_int, [C.POINTER(KfvmConfig), C.POINTER(KfvmIcParams), C.c_int,
                                    C.c_int, C.c_int, C.c_void_p]),
     ("kfvm_nccl_unique_id", C.c_int, [C.c_void_p]),
+    ("kfvm_loopback_id", C.c_int, [C.c_void_p]),
     ("kfvm_slab_range", None, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("kfvm_gpu_create", C.c_int, [C.POINTER(KfvmConfig), C.POINTER(KfvmTable), C.POINTER(KfvmDist),
                                   C.POINTER(C.c_void_p)]),

@@ -674,6 +674,8 @@ const int kNcclDouble = 8;  // ncclFloat64
 const int kNcclMax = 2;     // ncclMax
 }  // namespace
 
+#include "kfvm_loopback.cuh"
+
 // SSP(4,3) controller state (device)
 struct Ctl {
   double t, t_final, dt_err, err_prev, err;
@@ -727,6 +729,12 @@ struct kfvm_handle {
   cudaEvent_t ev[2];
   double t_states = 0, t_flux = 0, t_update = 0, t_other = 0;
   nccl_comm comm = nullptr;
+  // in-process loopback transport (kfvm_loopback_id): the ranks' handles
+  // live in one process on one device and exchange by device copies
+  kfvm_loop::Group* loop = nullptr;
+  unsigned long long loop_key = 0;
+  long long loop_op = -1;
+  std::vector<kfvm_loop::Pending> pend;
   long long launches = 0;
   long long graph_launches = 0;
   long long st_budget = 16LL << 30;
@@ -761,6 +769,50 @@ int fail(kfvm_handle* h, int code, const std::string& msg) {
     if (e_ != cudaSuccess)                                                            \
       return fail(h, KFVM_ERR_DEVICE, std::string(#x ": ") + cudaGetErrorString(e_)); \
   } while (0)
+
+// Slab-exchange transport: NCCL (one process per GPU) or the in-process
+// loopback group; point-to-point transfers are byte counts.
+int tx_start(kfvm_handle* h) {
+  if (h->loop) {
+    h->pend.clear();
+    return 0;
+  }
+  return nccl().GroupStart();
+}
+int tx_send(kfvm_handle* h, const void* p, size_t bytes, int peer, cudaStream_t st) {
+  if (h->loop) {
+    h->pend.push_back({true, const_cast<void*>(p), bytes, peer, st});
+    return 0;
+  }
+  return nccl().Send(p, bytes, kNcclUint8, peer, h->comm, st);
+}
+int tx_recv(kfvm_handle* h, void* p, size_t bytes, int peer, cudaStream_t st) {
+  if (h->loop) {
+    h->pend.push_back({false, p, bytes, peer, st});
+    return 0;
+  }
+  return nccl().Recv(p, bytes, kNcclUint8, peer, h->comm, st);
+}
+int tx_end(kfvm_handle* h) {
+  if (h->loop) {
+    const int rc = kfvm_loop::group_end(h->loop, h->rank, h->pend);
+    h->pend.clear();
+    return rc;
+  }
+  return nccl().GroupEnd();
+}
+int tx_allreduce_max_u64(kfvm_handle* h, unsigned long long* p, cudaStream_t st) {
+  if (h->loop) {
+    h->launches++;
+    return kfvm_loop::allreduce_max_u64(h->loop, h->rank, h->loop_op, p, st);
+  }
+  return nccl().AllReduce(p, p, 1, kNcclUint64, kNcclMax, h->comm, st);
+}
+int tx_allgather_f64(kfvm_handle* h, const double* src, double* dst, size_t count,
+                     cudaStream_t st) {
+  if (h->loop) return kfvm_loop::allgather_f64(h->loop, h->rank, h->loop_op, src, dst, count, st);
+  return nccl().AllGather(src, dst, count, kNcclDouble, h->comm, st);
+}
 
 // The constant banks (c_k, c_t, c_gather and the generated weight arrays of
 // kfvm_gen.cuh) are per device and shared by every handle on it.  A handle
@@ -1086,7 +1138,6 @@ int halo(kfvm_handle* h, double* U, cudaStream_t st) {
   if (!h->multi) {
     (void)per;  // k_ghost filled the halo planes
   } else {
-    NcclApi& N = nccl();
     const bool periodic = h->kc.per[h->dim - 1] != 0;
     const int lo = h->rank - 1, hi = h->rank + 1;
     const bool has_lo = periodic || lo >= 0, has_hi = periodic || hi < h->nranks;
@@ -1100,19 +1151,20 @@ int halo(kfvm_handle* h, double* U, cudaStream_t st) {
     // per peer pair the order is: upward transfer (my top interior -> the
     // upper rank's bottom halo), then downward; this keeps send/recv matching
     // correct when both neighbours are the same rank (2 ranks, periodic).
-    N.GroupStart();
+    const size_t bytes = (size_t)per * sizeof(double);
+    tx_start(h);
     for (int v = 0; v < h->nv; ++v) {
       double* base = U + (long long)v * h->g.vstride;
       double* top_int = base + (long long)h->g.np_loc * h->g.pstride;
       double* top_halo = base + (long long)(h->g.np_loc + h->g.H) * h->g.pstride;
       double* bot_int = base + per;
       double* bot_halo = base;
-      if (has_hi) N.Send(top_int, per, kNcclDouble, phi, h->comm, st);
-      if (has_lo) N.Recv(bot_halo, per, kNcclDouble, plo, h->comm, st);
-      if (has_lo) N.Send(bot_int, per, kNcclDouble, plo, h->comm, st);
-      if (has_hi) N.Recv(top_halo, per, kNcclDouble, phi, h->comm, st);
+      if (has_hi) tx_send(h, top_int, bytes, phi, st);
+      if (has_lo) tx_recv(h, bot_halo, bytes, plo, st);
+      if (has_lo) tx_send(h, bot_int, bytes, plo, st);
+      if (has_hi) tx_recv(h, top_halo, bytes, phi, st);
     }
-    if (N.GroupEnd() != 0) return fail(h, KFVM_ERR_DEVICE, "ncclGroupEnd failed");
+    if (tx_end(h) != 0) return fail(h, KFVM_ERR_DEVICE, "halo exchange failed");
   }
   toc(h, &h->t_other);
   return KFVM_OK;
@@ -1121,8 +1173,8 @@ int halo(kfvm_handle* h, double* U, cudaStream_t st) {
 int reduce_smax(kfvm_handle* h) {
   if (!h->multi) return KFVM_OK;
   // positive doubles order like their bit patterns: max on uint64 is exact
-  if (nccl().AllReduce(h->d_smax, h->d_smax, 1, kNcclUint64, kNcclMax, h->comm, h->stream) != 0)
-    return fail(h, KFVM_ERR_DEVICE, "ncclAllReduce failed");
+  if (tx_allreduce_max_u64(h, h->d_smax, h->stream) != 0)
+    return fail(h, KFVM_ERR_DEVICE, "allreduce (max wavespeed) failed");
   return KFVM_OK;
 }
 
@@ -1186,19 +1238,18 @@ int kx_flags(kfvm_handle* h, const double* U, const Chunk& ch) {
                                                               ch, h->p0, h->nsa);
   h->launches += 3;
   if (h->multi) {
-    NcclApi& N = nccl();
     const bool periodic = h->kc.per[h->dim - 1] != 0;
     const int lo = h->rank - 1, hi = h->rank + 1;
     const bool has_lo = periodic || lo >= 0, has_hi = periodic || hi < h->nranks;
     const int plo = (lo + h->nranks) % h->nranks, phi = hi % h->nranks;
     const long long pl = (long long)ch.ex * ch.em;
     unsigned char* f = h->d_flags;
-    N.GroupStart();
-    if (has_hi) N.Send(f + (long long)ch.C * pl, pl, kNcclUint8, phi, h->comm, h->stream);
-    if (has_lo) N.Recv(f, pl, kNcclUint8, plo, h->comm, h->stream);
-    if (has_lo) N.Send(f + pl, pl, kNcclUint8, plo, h->comm, h->stream);
-    if (has_hi) N.Recv(f + (long long)(ch.C + 1) * pl, pl, kNcclUint8, phi, h->comm, h->stream);
-    if (N.GroupEnd() != 0) return fail(h, KFVM_ERR_DEVICE, "ncclGroupEnd failed (flags)");
+    tx_start(h);
+    if (has_hi) tx_send(h, f + (long long)ch.C * pl, pl, phi, h->stream);
+    if (has_lo) tx_recv(h, f, pl, plo, h->stream);
+    if (has_lo) tx_send(h, f + pl, pl, plo, h->stream);
+    if (has_hi) tx_recv(h, f + (long long)(ch.C + 1) * pl, pl, phi, h->stream);
+    if (tx_end(h) != 0) return fail(h, KFVM_ERR_DEVICE, "flag exchange failed");
   }
   k_kx_mirror<DIM><<<blocks(ch.next, 256), 256, 0, h->stream>>>(h->d_flags, h->g, ch, h->p0,
                                                                 h->nsa, h->multi ? 1 : 0);
@@ -1445,8 +1496,8 @@ int enqueue_attempt43(kfvm_handle* h) {
                                                        nrow, np);
   h->launches += 2;
   if (h->multi) {
-    if (nccl().AllGather(loc, h->d_planes, (size_t)h->npmax, kNcclDouble, h->comm, h->stream) != 0)
-      return fail(h, KFVM_ERR_DEVICE, "ncclAllGather failed (error norm)");
+    if (tx_allgather_f64(h, loc, h->d_planes, (size_t)h->npmax, h->stream) != 0)
+      return fail(h, KFVM_ERR_DEVICE, "allgather (error norm) failed");
   }
   const double ncomp = (double)h->g.nx * h->g.nm * h->nsa * h->nv;
   k_ctl43<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_planes, h->d_nps, h->nranks, h->npmax, ncomp,
@@ -1680,6 +1731,11 @@ extern "C" int kfvm_nccl_unique_id(unsigned char id[128]) {
   nccl_uid u;
   if (N.GetUniqueId(&u) != 0) return KFVM_ERR_DEVICE;
   std::memcpy(id, u.internal, 128);
+  return KFVM_OK;
+}
+
+extern "C" int kfvm_loopback_id(unsigned char id[128]) {
+  kfvm_loop::make_id(id);
   return KFVM_OK;
 }
 
@@ -1992,7 +2048,14 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   bad(cudaEventCreate(&h->ev[0]), "event");
   bad(cudaEventCreate(&h->ev[1]), "event");
   if (rc == KFVM_OK) rc = ensure_dt_cap(h, 1024);
-  if (rc == KFVM_OK && h->multi) {
+  if (rc == KFVM_OK && h->multi && dist && kfvm_loop::is_id(dist->nccl_id)) {
+    h->loop_key = kfvm_loop::id_key(dist->nccl_id);
+    h->loop = kfvm_loop::join(h->loop_key, h->nranks, h->device);
+    if (!h->loop) {
+      rc = KFVM_ERR_CONFIG;
+      h->err = "loopback group: rank count or device differs from the group's";
+    }
+  } else if (rc == KFVM_OK && h->multi) {
     NcclApi& N = nccl();
     if (!N.ok) {
       rc = KFVM_ERR_DEVICE;
@@ -2023,6 +2086,7 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
   if (h->graph) cudaGraphExecDestroy(h->graph);
   if (h->graph43) cudaGraphExecDestroy(h->graph43);
   if (h->comm) nccl().CommDestroy(h->comm);
+  if (h->loop) kfvm_loop::leave(h->loop_key, h->loop);
   cudaSetDevice(h->device);
   if (h->registered) {
     std::lock_guard<std::mutex> lk(g_image_mu);
@@ -2274,7 +2338,7 @@ int run_steps(kfvm_handle* h, int nsteps, bool reset) {
   }
   int rc = enqueue_speed(h);
   if (rc) return rc;
-  if (h->timing || h->multi) {
+  if (h->timing || h->loop) {  // loopback rendezvous is host-side: not capturable
     for (int s = 0; s < nsteps; ++s)
       if ((rc = enqueue_step(h))) return rc;
     return KFVM_OK;
@@ -2348,7 +2412,7 @@ int advance43(kfvm_handle* h, double t_final, int max_attempts, int* steps, doub
   c0.err_prev = 1.0;
   CK(cudaMemcpyAsync(h->d_ctl, &c0, sizeof(c0), cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
-  if (!h->graph43) {
+  if (!h->graph43 && !h->loop) {
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     const long long l0 = h->launches;
@@ -2365,8 +2429,15 @@ int advance43(kfvm_handle* h, double t_final, int max_attempts, int* steps, doub
   int attempts = 0;
   while (attempts < max_attempts) {
     const int n = std::min(8, max_attempts - attempts);
-    for (int i = 0; i < n; ++i) CK(cudaGraphLaunch(h->graph43, h->stream));
-    h->launches += h->graph43_launches * n;
+    for (int i = 0; i < n; ++i) {
+      if (h->loop) {
+        const int rc = enqueue_attempt43(h);
+        if (rc) return rc;
+      } else {
+        CK(cudaGraphLaunch(h->graph43, h->stream));
+        h->launches += h->graph43_launches;
+      }
+    }
     attempts += n;
     CK(cudaMemcpyAsync(&c, h->d_ctl, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));

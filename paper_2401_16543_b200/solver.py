@@ -246,3 +246,12 @@ def nccl_unique_id() -> bytes:
     if rc:
         raise KfvmDeviceError("ncclGetUniqueId failed (libnccl.so.2 not loadable?)")
     return bytes(buf)
+
+
+def loopback_id() -> bytes:
+    """Group id of the in-process loopback transport (kfvm_loopback_id): the
+    nranks Solver handles created with it in this process (same device, one
+    host thread per rank) exchange halos and reductions by device copies."""
+    buf = (C.c_ubyte * 128)()
+    _abi.lib().kfvm_loopback_id(buf)
+    return bytes(buf)
