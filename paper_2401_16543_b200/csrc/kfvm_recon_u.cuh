@@ -30,6 +30,9 @@ constexpr int kUChunkUnroll = KFVM_U_UNR;
 #ifndef KFVM_U_MINB
 #define KFVM_U_MINB 2
 #endif
+#ifndef KFVM_U_EXTRA_SMEM  // occupancy experiments: padding per CTA (bytes)
+#define KFVM_U_EXTRA_SMEM 0
+#endif
 #ifndef KFVM_U_BSMEM_MAX
 #define KFVM_U_BSMEM_MAX (48 * 1024)
 #endif
@@ -65,7 +68,7 @@ struct UCfg {
   static constexpr int NG = (NPT + PG - 1) / PG;         // groups (>1: limiter separate)
   static constexpr size_t bytes() {
     return sizeof(double) * (RING * PL + PRING * PPL + 4 * SCW + SB) +
-           sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK);
+           sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK) + KFVM_U_EXTRA_SMEM;
   }
 };
 
