@@ -1687,6 +1687,34 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
       }
     }
   }
+  if constexpr (M::PK) {
+    // pass 2 packed: the NTOT stencil slots in stencil order, 4 per chunk,
+    // zero B (pads) only in the last chunk; slot word = region offset |
+    // (z offset + R) << 9 | stencil << 12
+    const size_t b0 = bf.size();
+    bf.resize(b0 + (size_t)M::NCH2 * M::NPT * 32, 0.0);
+    const size_t g0 = g4.size();
+    g4.resize(g0 + (size_t)M::NCH2 * 4, 0);
+    int sl = 0;
+    for (int q = 0; q < G::NS; ++q) {
+      const int N = t->size[q], o = t->cell_offset[q];
+      for (int hh = 0; hh < N; ++hh, ++sl) {
+        const int ck = sl / 4, k = sl % 4;
+        const int e = t->gather[o + hh];
+        const int inpl = (G::OFF[e][1] + R) * M::RX + G::OFF[e][0] + R;
+        g4[g0 + sl] = inpl | ((G::OFF[e][2] + R) << 9) | (q << 12);
+        for (int col = 0; col < 8; ++col)
+          for (int n = 0; n < M::NPT; ++n) {
+            const int sp = 8 * n + col;
+            bf[b0 + ((size_t)ck * M::NPT + n) * 32 + col * 4 + k] =
+                sp < G::NP ? t->face[(size_t)o * G::NP + (size_t)sp * N + hh] : 0.0;
+          }
+      }
+    }
+    for (; sl < 4 * M::NCH2; ++sl) {  // trailing pads: any valid slot, zero weights
+      g4[g0 + sl] = g4[g0 + sl - 1];
+    }
+  }
   if constexpr (D == 3) {
     // the fused 3-D engine's region geometry (8 x 4 tile): same chunks and slots
     std::vector<int> g8(g4);

@@ -64,11 +64,14 @@ struct UCfg {
       !(D == 3 && R == 2) && G::NCHUNK * (ND + NPT) * 32 * 8 <= KFVM_U_BSMEM_MAX;
   static constexpr int MINB = D == 3 ? (R == 2 ? 3 : KFVM_U_MINB) : 4;
   static constexpr int SB = BSMEM ? G::NCHUNK * (ND + NPT) * 32 : 0;  // B fragments
+  // 3-D: pass 2 over chunks packed across stencil boundaries
+  static constexpr bool PK = D == 3;
+  static constexpr int NCH2 = PK ? (G::NTOT + 3) / 4 : 0;
   static constexpr int PG = NPT <= 3 ? NPT : 4;         // point tiles per pass-2 group
   static constexpr int NG = (NPT + PG - 1) / PG;         // groups (>1: limiter separate)
   static constexpr size_t bytes() {
     return sizeof(double) * (RING * PL + PRING * PPL + 4 * SCW + SB) +
-           sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK) + KFVM_U_EXTRA_SMEM;
+           sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK + 4 * NCH2) + KFVM_U_EXTRA_SMEM;
   }
 };
 
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int k4 = lane & 3, r8 = lane >> 2;
   // chunk tables (host-built): region offset and z offset of every chunk slot
-  for (int i = threadIdx.x; i < 9 * G::NCHUNK; i += 128) sTab[i] = gat4[i];
+  for (int i = threadIdx.x; i < 9 * G::NCHUNK + 4 * C::NCH2; i += 128) sTab[i] = gat4[i];
   if constexpr (C::BSMEM) {
     for (int i = threadIdx.x; i < G::NCHUNK * ND * 32; i += 128) sBd[i] = __ldg(Bd + i);
     for (int i = threadIdx.x; i < G::NCHUNK * NPT * 32; i += 128) sBf[i] = __ldg(Bf + i);
@@ -385,28 +388,58 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
       double cq[nv];
 #pragma unroll
       for (int v = 0; v < nv; ++v) cq[v] = P1 ? 1.0 : sCw[v * 8 + r8];
-      constexpr int NCK = P1 ? G::kc(0) : G::NCHUNK;  // pass 1: stencil 0 only
+      // 3-D: the chunks of pass 2 are packed across stencil boundaries (C::PK:
+      // no per-stencil zero padding; a pad is an exact no-op of the chain, so
+      // the bits are unchanged) and each slot carries its own stencil, whose
+      // c_q the lane reloads when it changes
+      constexpr bool PK = C::PK && !P1;
+      constexpr int NCK = P1 ? G::kc(0) : (PK ? C::NCH2 : G::NCHUNK);  // pass 1: stencil 0 only
+      const int* sT2 = sTab + 9 * G::NCHUNK;
+      const double* Bf2 = Bf + G::NCHUNK * NPT * 32;
+      auto slot = [&](int ck, int& inpl, int& ozr, int& qs) {
+        if constexpr (PK) {
+          const int pk = sT2[ck * 4 + k4];
+          inpl = pk & 511;
+          ozr = (pk >> 9) & 7;
+          qs = pk >> 12;
+        } else {
+          inpl = sTab[2 * (ck * 4 + k4)];
+          ozr = sTab[2 * (ck * 4 + k4) + 1] + R;
+          qs = 0;
+        }
+      };
+      auto bfrag = [&](int ck, int n) -> double {
+        if constexpr (PK) return ldB2(Bf2 + (ck * NPT + n) * 32 + lane);
+        return Bfp[(ck * NPT + n) * 32 + lane];
+      };
+      int qa = 0, qcur = 0;
       // software pipeline: fragments of chunk ck+1 load while chunk ck issues
       double av[nv], bv[PG];
       {
-        const int inpl = sTab[2 * k4], oz = sTab[2 * k4 + 1];
-        const double* ap = plane(oz + R) + inpl + cidx;
+        int inpl, ozr;
+        slot(0, inpl, ozr, qa);
+        const double* ap = plane(ozr) + inpl + cidx;
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = ap[u * C::RROW];
 #pragma unroll
-        for (int n = 0; n < PG; ++n) bv[n] = t0 + n < NPT ? Bfp[(t0 + n) * 32 + lane] : 0.0;
+        for (int n = 0; n < PG; ++n) bv[n] = t0 + n < NPT ? bfrag(0, t0 + n) : 0.0;
       }
 #pragma unroll kUChunkUnroll
       for (int ck = 0; ck < NCK; ++ck) {
         const int cn = ck + 1 < NCK ? ck + 1 : ck;
-        const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
-        const double* ap = plane(oz + R) + inpl + cidx;
+        int inpl, ozr, qn;
+        slot(cn, inpl, ozr, qn);
+        const double* ap = plane(ozr) + inpl + cidx;
         double an[nv], bn[PG];
 #pragma unroll
         for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
 #pragma unroll
-        for (int n = 0; n < PG; ++n)
-          bn[n] = t0 + n < NPT ? Bfp[(cn * NPT + t0 + n) * 32 + lane] : 0.0;
+        for (int n = 0; n < PG; ++n) bn[n] = t0 + n < NPT ? bfrag(cn, t0 + n) : 0.0;
+        if (PK && qa != qcur) {  // this slot starts a new stencil
+          qcur = qa;
+#pragma unroll
+          for (int v = 0; v < nv; ++v) cq[v] = sCw[(qcur * nv + v) * 8 + r8];
+        }
         double aw[nv];  // c_q (Phi U)_v at the slot, with this lane's cell's Phi
 #pragma unroll
         for (int v = 0; v < nv; ++v) aw[v] = P1 ? av[v] : cq[v] * phi_row<D>(T, av, v);
@@ -419,7 +452,8 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
         for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
         for (int n = 0; n < PG; ++n) bv[n] = bn[n];
-        if (!P1 && (sQ[ck] & 256) && q + 1 < NS) {
+        qa = qn;
+        if (!P1 && !PK && (sQ[ck] & 256) && q + 1 < NS) {
           ++q;
 #pragma unroll
           for (int v = 0; v < nv; ++v) cq[v] = sCw[(q * nv + v) * 8 + r8];
