@@ -48,7 +48,7 @@ namespace kfvm_b200 {
 #define KFVM_FLUX_MINB2 8
 #endif
 #ifndef KFVM_FLUX_MINB3
-#define KFVM_FLUX_MINB3 5
+#define KFVM_FLUX_MINB3 4
 #endif
 __constant__ DevConsts c_k;
 __constant__ DevTable c_t;
@@ -207,8 +207,12 @@ __device__ __forceinline__ void face_flux(const double* __restrict__ St, double*
   for (int v = 0; v < nv; ++v) F[(long long)(d * nv + v) * ch.nfb + f] = Fb[v];
 }
 
-// one thread per face of direction d = blockIdx.y; min blocks per SM
-// measured on config 2 (8) and config 3 (5: no spills, 11.7 vs 12.6 ms/step at 6)
+// one thread per face of direction d = blockIdx.y; min blocks per SM: 3-D 4
+// (116-118 registers, no spills; 5 spilled 336 B at the same speed, 6 was
+// slower); 2-D 8: 64 registers with 368 B (R=2) / 776 B (R=3) of spills —
+// the HLLC solve alone needs more than 64 registers, and the 0-spill build
+// (94 registers, 5 CTAs/SM) was slower on config 2 (1.36 vs 1.34 ms/step;
+// profiles/r02/README.md)
 template <int DIM, int R>
 __global__ void __launch_bounds__(128, DIM == 2 ? KFVM_FLUX_MINB2 : KFVM_FLUX_MINB3) k_flux(const double* __restrict__ St,
                                                               double* __restrict__ F, Geo g,
