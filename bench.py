@@ -201,17 +201,19 @@ def run_reference(args, w, rank):
 
 def traffic_of(config_index, shape):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture of this exact workload (profiles/r01/roofline_traffic.json), or
-    None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
-            t = json.load(f)[str(config_index)]
+    capture of this exact workload (profiles/r02/roofline_traffic.json, else
+    the round-1 capture profiles/r01/roofline_traffic.json), or None."""
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "roofline_traffic.json")) as f:
+                t = json.load(f)[str(config_index)]
+        except Exception:
+            continue
         if list(t["shape"]) != list(shape):
-            return None, None
+            continue
         return (t["dram_read_bytes"] + t["dram_write_bytes"],
-                "dram read+write bytes per launch, ncu --set full: profiles/r01/" + t["capture"])
-    except Exception:
-        return None, None
+                f"dram read+write bytes per launch, ncu --set full: profiles/{rnd}/" + t["capture"])
+    return None, None
 
 
 def workload_config(w, args):
