@@ -701,6 +701,7 @@ struct kfvm_handle {
   double *U0 = nullptr, *Ua = nullptr, *Ub = nullptr;
   double* Pr = nullptr;  // k_prims output: p, c, 1/rho, u_d per cell (incl. halos)
   double *St = nullptr, *F = nullptr, *aos = nullptr;
+  double* Lb = nullptr;  // 3-D R=2 tensor engine: limiter bounds [3][extended cell] (inside St)
   size_t st_elems = 0, f_elems = 0, aos_elems = 0;
   int chunk = 0;
   int ring_split = 1;  // option "ring_split": ring columns by k_states_fast
@@ -973,8 +974,14 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
     const int KZ = h->kz;
     const long long nblk2 =
         (long long)((ch.ex - 2 * xsp + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
-    k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(), h->stream>>>(
-        U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, nullptr, xsp);
+    constexpr bool LB = DIM == 3 && R == 2;
+    if (LB) {
+      k_bounds<DIM><<<blocks(ext_range(ch), 256), 256, 0, h->stream>>>(U, h->Pr, h->Lb, h->g, ch,
+                                                                       h->d_err);
+      h->launches++;
+    }
+    k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(LB), h->stream>>>(
+        U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, nullptr, xsp, h->Lb);
     ring();
     dbg_sync(h, "k_states_u");
     if (UCfg<DIM, R>::NG > 1) {
@@ -1592,10 +1599,11 @@ int configure_scratch(kfvm_handle* h, long long chunk_planes) {
     set_ranges(h, 1, &r0, &r1);
     return KFVM_OK;
   }
+  const int nlb = (h->dim == 3 && h->R == 2) ? 3 : 0;  // k_bounds output per extended cell
   const long long per_plane =
-      ((long long)(h->g.nx + 2) * (h->dim == 3 ? h->g.nm + 2 : 1) * h->NP +
-       (long long)(h->g.nx + 1) * (h->dim == 3 ? h->g.nm + 1 : 1) * h->dim) *
-      h->nv * (long long)sizeof(double);
+      ((long long)(h->g.nx + 2) * (h->dim == 3 ? h->g.nm + 2 : 1) * (h->NP * h->nv + nlb) +
+       (long long)(h->g.nx + 1) * (h->dim == 3 ? h->g.nm + 1 : 1) * h->dim * h->nv) *
+      (long long)sizeof(double);
   long long c = chunk_planes;
   if (c <= 0) {
     size_t fr = 0, tot = 0;
@@ -1613,8 +1621,9 @@ int configure_scratch(kfvm_handle* h, long long chunk_planes) {
   const Chunk ch = make_chunk(h, 0, h->chunk);
   h->st_elems = (size_t)ch.next * h->NP * h->nv;
   h->f_elems = (size_t)ch.nfb * h->dim * h->nv;
-  CK(cudaMalloc(&h->St, h->st_elems * sizeof(double)));
+  CK(cudaMalloc(&h->St, (h->st_elems + (size_t)ch.next * nlb) * sizeof(double)));
   CK(cudaMalloc(&h->F, h->f_elems * sizeof(double)));
+  h->Lb = nlb ? h->St + h->st_elems : nullptr;
   return KFVM_OK;
 }
 
@@ -1746,7 +1755,7 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   CK(cudaMemcpy(h->d_Bf, bf.data(), bf.size() * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_gat4, g4.data(), g4.size() * sizeof(int), cudaMemcpyHostToDevice));
   CK(cudaFuncSetAttribute(k_states_u<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)M::bytes()));
+                          (int)M::bytes(D == 3 && R == 2)));
   CK(cudaFuncSetAttribute(k_states_u<D, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)M::bytes()));
   CK(cudaFuncSetAttribute(k_states_u<D, R, false, true>,

@@ -30,6 +30,13 @@ constexpr int kUChunkUnroll = KFVM_U_UNR;
 #ifndef KFVM_U_MINB
 #define KFVM_U_MINB 2
 #endif
+// 3-D R=2: 4 CTAs/SM (128 registers, 32 B of spills) now that the limiter
+// bounds come from k_bounds and the shared memory is 54.9 KB per CTA —
+// measured 121.7 vs 125.3 ms/step (config 3) and 961.9 vs 994.4 (config 4)
+// against 3 CTAs at 166 registers (profiles/r02/README.md)
+#ifndef KFVM_U_MINB32
+#define KFVM_U_MINB32 4
+#endif
 #ifndef KFVM_U_EXTRA_SMEM  // occupancy experiments: padding per CTA (bytes)
 #define KFVM_U_EXTRA_SMEM 0
 #endif
@@ -62,15 +69,17 @@ struct UCfg {
   // faster than 2 CTAs with B in shared memory, profiles/r01/README.md)
   static constexpr bool BSMEM =
       !(D == 3 && R == 2) && G::NCHUNK * (ND + NPT) * 32 * 8 <= KFVM_U_BSMEM_MAX;
-  static constexpr int MINB = D == 3 ? (R == 2 ? 3 : KFVM_U_MINB) : 4;
+  static constexpr int MINB = D == 3 ? (R == 2 ? KFVM_U_MINB32 : KFVM_U_MINB) : 4;
   static constexpr int SB = BSMEM ? G::NCHUNK * (ND + NPT) * 32 : 0;  // B fragments
   // 3-D: pass 2 over chunks packed across stencil boundaries
   static constexpr bool PK = D == 3;
   static constexpr int NCH2 = PK ? (G::NTOT + 3) / 4 : 0;
   static constexpr int PG = NPT <= 3 ? NPT : 4;         // point tiles per pass-2 group
   static constexpr int NG = (NPT + PG - 1) / PG;         // groups (>1: limiter separate)
-  static constexpr size_t bytes() {
-    return sizeof(double) * (RING * PL + PRING * PPL + 4 * SCW + SB) +
+  // LB: the instance whose limiter bounds come from k_bounds (3-D R=2 main
+  // engine): no per-cell-quantity ring in shared memory
+  static constexpr size_t bytes(bool lb = false) {
+    return sizeof(double) * (RING * PL + (lb ? 0 : PRING * PPL) + 4 * SCW + SB) +
            sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK + 4 * NCH2) + KFVM_U_EXTRA_SMEM;
   }
 };
@@ -96,14 +105,17 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
                double* __restrict__ St, Geo g, Chunk ch, int KZ, int* __restrict__ err,
                const double* __restrict__ Bd, const double* __restrict__ Bf,
                const int* __restrict__ gat4, const unsigned char* __restrict__ kfl = nullptr,
-               int xsp = 0) {
+               int xsp = 0, const double* __restrict__ Lb = nullptr) {
   using G = Gen<D, R>;
   using C = UCfg<D, R>;
+  // LB: per-cell limiter bounds {rho_max, rho_min, p_min} from k_bounds and
+  // the transform's per-cell quantities from Pr in global memory (no ring)
+  constexpr bool LB = D == 3 && R == 2 && !P1 && !KXM && C::NG == 1;
   constexpr int nv = C::nv, NP = G::NP, NS = G::NS, ND = C::ND, NPT = C::NPT;
   extern __shared__ double smem[];
   double* sRing = smem;                          // [RING][nv][RY][RX]
   double* sPr = sRing + C::RING * C::PL;         // [PRING][NF][NY][NX]
-  double* sC = sPr + C::PRING * C::PPL;          // [warp][q][v][8]
+  double* sC = sPr + (LB ? 0 : C::PRING * C::PPL);  // [warp][q][v][8]
   double* sBd = sC + 4 * C::SCW;                 // B fragments [chunk][n][lane]
   double* sBf = sBd + G::NCHUNK * ND * 32;
   int* sTab = reinterpret_cast<int*>(sBd + C::SB);  // [chunk][4] {inplane, oz}
@@ -175,7 +187,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
   {
     const int p = ch.c0 - 1 + cstart;
     for (int oz = -R; oz <= R; ++oz) load_plane(p + oz);
-    if (!P1)  // pass 1 needs neither the transform nor the limiter statistics
+    if (!P1 && !LB)  // pass 1 needs neither the transform nor the limiter statistics
       for (int oz = -1; oz <= 1; ++oz) load_prims(p + oz);
     __pipeline_commit();
     __pipeline_wait_prior(0);
@@ -188,7 +200,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     const int p = ch.c0 - 1 + c;
     if (c + 1 < cend) {
       load_plane(p + R + 1);
-      if (!P1) load_prims(p + 2);
+      if (!P1 && !LB) load_prims(p + 2);
     }
     __pipeline_commit();
     // KXRCF: the WENO passes run only for planes of this segment holding a
@@ -217,11 +229,14 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     // ---- transform of the cell average (identical to d_make_transform)
     DTransform T;
     T.rt = plane(R)[icr];
-    T.inv_r = pr0[2 * C::PROW + icn];
+    // LB: the cell's per-cell quantities straight from Pr (the quad's lanes
+    // load the same words)
+    const long long icg = LB ? uidx<D>(g, a - 1, j, p) : 0;
+    T.inv_r = LB ? __ldg(Pr + 2 * g.vstride + icg) : pr0[2 * C::PROW + icn];
     T.ut[2] = T.mt[2] = 0.0;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      T.ut[d] = pr0[(3 + d) * C::PROW + icn];
+      T.ut[d] = LB ? __ldg(Pr + (3 + d) * g.vstride + icg) : pr0[(3 + d) * C::PROW + icn];
       T.mt[d] = plane(R)[(1 + d) * C::RROW + icr];
     }
     {
@@ -508,45 +523,56 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
       }
     // ---- positivity limiter: neighbourhood statistics, the 4
     // lanes of the quad split the 3^d neighbours and reduce (max/min exact)
-    double rbmax = T.rt, rbmin = T.rt, pbmin = pr0[icn], cmin = pr0[C::PROW + icn];
-    {
-      constexpr int NN = D == 3 ? 27 : 9;
-      for (int m = k4; m < NN; m += 4) {
-        const int aa = m % 3 - 1;
-        const int bb = D == 3 ? (m / 3) % 3 - 1 : 0;
-        const int cc = D == 3 ? m / 9 - 1 : m / 3 - 1;
-        const double r = plane(R + cc)[(D == 3 ? bb * C::RX : 0) + icr + aa];
-        const double* prz = cc < 0 ? prm : (cc > 0 ? prp : pr0);
-        const int ip = (D == 3 ? bb * C::NX : 0) + icn + aa;
-        rbmax = fmax(rbmax, r);
-        rbmin = fmin(rbmin, r);
-        pbmin = fmin(pbmin, prz[ip]);
-        cmin = fmin(cmin, prz[C::PROW + ip]);
-      }
-#pragma unroll
-      for (int o = 1; o <= 2; o <<= 1) {
-        rbmax = fmax(rbmax, __shfl_xor_sync(0xffffffffu, rbmax, o));
-        rbmin = fmin(rbmin, __shfl_xor_sync(0xffffffffu, rbmin, o));
-        pbmin = fmin(pbmin, __shfl_xor_sync(0xffffffffu, pbmin, o));
-        cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
-      }
-    }
-    double delta = 0.5 * (pr0[3 * C::PROW + icn + 1] - pr0[3 * C::PROW + icn - 1]);
-    if (D == 3) {
-      delta = fma(0.5, pr0[4 * C::PROW + icn + C::NX] - pr0[4 * C::PROW + icn - C::NX], delta);
-      delta = fma(0.5, prp[5 * C::PROW + icn] - prm[5 * C::PROW + icn], delta);
+    double rmax, rmin, pmin;
+    if constexpr (LB) {
+      const long long tidb = ((long long)c * ch.em + b) * ch.ex + a;
+      rmax = __ldg(Lb + tidb);
+      rmin = __ldg(Lb + ch.next + tidb);
+      pmin = __ldg(Lb + 2 * ch.next + tidb);
     } else {
-      delta = fma(0.5, prp[4 * C::PROW + icn] - prm[4 * C::PROW + icn], delta);
+      double rbmax = T.rt, rbmin = T.rt, pbmin = pr0[icn], cmin = pr0[C::PROW + icn];
+      {
+        constexpr int NN = D == 3 ? 27 : 9;
+        for (int m = k4; m < NN; m += 4) {
+          const int aa = m % 3 - 1;
+          const int bb = D == 3 ? (m / 3) % 3 - 1 : 0;
+          const int cc = D == 3 ? m / 9 - 1 : m / 3 - 1;
+          const double r = plane(R + cc)[(D == 3 ? bb * C::RX : 0) + icr + aa];
+          const double* prz = cc < 0 ? prm : (cc > 0 ? prp : pr0);
+          const int ip = (D == 3 ? bb * C::NX : 0) + icn + aa;
+          rbmax = fmax(rbmax, r);
+          rbmin = fmin(rbmin, r);
+          pbmin = fmin(pbmin, prz[ip]);
+          cmin = fmin(cmin, prz[C::PROW + ip]);
+        }
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+          rbmax = fmax(rbmax, __shfl_xor_sync(0xffffffffu, rbmax, o));
+          rbmin = fmin(rbmin, __shfl_xor_sync(0xffffffffu, rbmin, o));
+          pbmin = fmin(pbmin, __shfl_xor_sync(0xffffffffu, pbmin, o));
+          cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+        }
+      }
+      double delta = 0.5 * (pr0[3 * C::PROW + icn + 1] - pr0[3 * C::PROW + icn - 1]);
+      if (D == 3) {
+        delta = fma(0.5, pr0[4 * C::PROW + icn + C::NX] - pr0[4 * C::PROW + icn - C::NX], delta);
+        delta = fma(0.5, prp[5 * C::PROW + icn] - prm[5 * C::PROW + icn], delta);
+      } else {
+        delta = fma(0.5, prp[4 * C::PROW + icn] - prm[4 * C::PROW + icn], delta);
+      }
+      const double kc = c_k.kf * cmin;
+      double eta = -(delta + kc) / kc;
+      eta = fmin(1.0, fmax(0.0, eta));
+      const double fup = fma(c_k.kappa, 1.0 - eta, 1.0);
+      const double flo = fma(-c_k.kappa, 1.0 - eta, 1.0);
+      rmax = rbmax * fup;
+      rmin = rbmin * flo;
+      pmin = pbmin * flo;
+      const double rt = T.rt, pt = pr0[icn];
+      if (!(rt > 0.0) || !(pt > 0.0) || !(rmin > 0.0) || !(pmin > 0.0))
+        if (active && k4 == 0) atomicOr(err, 2);
     }
-    const double kc = c_k.kf * cmin;
-    double eta = -(delta + kc) / kc;
-    eta = fmin(1.0, fmax(0.0, eta));
-    const double fup = fma(c_k.kappa, 1.0 - eta, 1.0);
-    const double flo = fma(-c_k.kappa, 1.0 - eta, 1.0);
-    const double rmax = rbmax * fup, rmin = rbmin * flo, pmin = pbmin * flo;
-    const double rt = T.rt, pt = pr0[icn];
-    if (!(rt > 0.0) || !(pt > 0.0) || !(rmin > 0.0) || !(pmin > 0.0))
-      if (active && k4 == 0) atomicOr(err, 2);
+    const double rt = T.rt;
     double Ubar[nv];
     Ubar[0] = rt;
 #pragma unroll
@@ -694,6 +720,63 @@ __global__ void __launch_bounds__(128) k_limit_states(const double* __restrict__
         if (thp < 1.0) u = fma(thp, u - Ubar[v], Ubar[v]);
         *q = u;
       }
+}
+
+// ------------------------------------------------------------- k_bounds
+// Positivity-limiter bounds of every extended cell of the plane range
+// [e0, e1) (the same operations as the in-kernel statistics of
+// k_states_u and k_limit_states): rho_max, rho_min, p_min into
+// Lb[3][extended cell], and the admissibility check of the average.  The
+// 3-D R=2 tensor engine reads them instead of keeping a ring of per-cell
+// quantities in shared memory.
+template <int D>
+__global__ void __launch_bounds__(256) k_bounds(const double* __restrict__ U,
+                                                const double* __restrict__ Pr,
+                                                double* __restrict__ Lb, Geo g, Chunk ch,
+                                                int* __restrict__ err) {
+  const long long tid = (long long)ch.e0 * ch.ex * ch.em + (long long)blockIdx.x * 256 + threadIdx.x;
+  if (tid >= (long long)ch.e1 * ch.ex * ch.em) return;
+  const int a = (int)(tid % ch.ex);
+  const long long r1 = tid / ch.ex;
+  const int b = (int)(r1 % ch.em), c = (int)(r1 / ch.em);
+  const int x = a - 1, j = D == 3 ? b - 1 : 0, p = ch.c0 - 1 + c;
+  const long long ic = uidx<D>(g, x, j, p);
+  const double rt = __ldg(U + ic), pt = __ldg(Pr + ic);
+  double rbmax = rt, rbmin = rt, pbmin = pt, cmin = __ldg(Pr + g.vstride + ic);
+#pragma unroll
+  for (int cc = -1; cc <= 1; ++cc)
+#pragma unroll
+    for (int bb = (D == 3 ? -1 : 0); bb <= (D == 3 ? 1 : 0); ++bb)
+#pragma unroll
+      for (int aa = -1; aa <= 1; ++aa) {
+        const long long o = uidx<D>(g, x + aa, j + bb, p + cc);
+        const double r = __ldg(U + o);
+        rbmax = fmax(rbmax, r);
+        rbmin = fmin(rbmin, r);
+        pbmin = fmin(pbmin, __ldg(Pr + o));
+        cmin = fmin(cmin, __ldg(Pr + g.vstride + o));
+      }
+  double delta = 0.5 * (__ldg(Pr + 3 * g.vstride + uidx<D>(g, x + 1, j, p)) -
+                        __ldg(Pr + 3 * g.vstride + uidx<D>(g, x - 1, j, p)));
+  if (D == 3) {
+    delta = fma(0.5, __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j + 1, p)) -
+                         __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j - 1, p)), delta);
+    delta = fma(0.5, __ldg(Pr + 5 * g.vstride + uidx<D>(g, x, j, p + 1)) -
+                         __ldg(Pr + 5 * g.vstride + uidx<D>(g, x, j, p - 1)), delta);
+  } else {
+    delta = fma(0.5, __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j, p + 1)) -
+                         __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j, p - 1)), delta);
+  }
+  const double kc = c_k.kf * cmin;
+  double eta = -(delta + kc) / kc;
+  eta = fmin(1.0, fmax(0.0, eta));
+  const double fup = fma(c_k.kappa, 1.0 - eta, 1.0);
+  const double flo = fma(-c_k.kappa, 1.0 - eta, 1.0);
+  const double rmax = rbmax * fup, rmin = rbmin * flo, pmin = pbmin * flo;
+  if (!(rt > 0.0) || !(pt > 0.0) || !(rmin > 0.0) || !(pmin > 0.0)) atomicOr(err, 2);
+  Lb[tid] = rmax;
+  Lb[ch.next + tid] = rmin;
+  Lb[2 * ch.next + tid] = pmin;
 }
 
 #endif
