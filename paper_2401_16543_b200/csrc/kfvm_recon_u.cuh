@@ -228,7 +228,15 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     const int icr = (D == 3 ? R * C::RX : 0) + xr;      // cell centre in a region plane
     // ---- transform of the cell average (identical to d_make_transform)
     DTransform T;
-    T.rt = plane(R)[icr];
+    // rho~ and m~ enter only Phi^-1 (after pass 2): with one point group they
+    // are read from the ring there, out of the passes' register budget
+    constexpr bool LATE_RM = C::NG == 1 && !KXM && !P1;
+    auto load_rm = [&]() {
+      T.rt = plane(R)[icr];
+#pragma unroll
+      for (int d = 0; d < D; ++d) T.mt[d] = plane(R)[(1 + d) * C::RROW + icr];
+    };
+    if (!LATE_RM) load_rm();
     // LB: the cell's per-cell quantities straight from Pr (the quad's lanes
     // load the same words)
     const long long icg = LB ? uidx<D>(g, a - 1, j, p) : 0;
@@ -237,7 +245,6 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       T.ut[d] = LB ? __ldg(Pr + (3 + d) * g.vstride + icg) : pr0[(3 + d) * C::PROW + icn];
-      T.mt[d] = plane(R)[(1 + d) * C::RROW + icr];
     }
     {
       double ke = T.ut[0] * T.ut[0];
@@ -510,6 +517,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     PHASE_MARK(3);
     if constexpr (NG == 1 && !P1 && !KXM) {
     {
+    if (LATE_RM) load_rm();
     // ---- Phi^-1: conservative states at this lane's points s = 8n + 2k4 + e
     double st[NPT][2][nv];
 #pragma unroll
