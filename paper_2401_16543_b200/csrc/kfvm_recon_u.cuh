@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     constexpr bool LATE_RM = C::NG == 1 && !KXM && !P1;
     auto load_rm = [&]() {
       T.rt = plane(R)[icr];
+      T.mt[2] = 0.0;
 #pragma unroll
       for (int d = 0; d < D; ++d) T.mt[d] = plane(R)[(1 + d) * C::RROW + icr];
     };
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
     // load the same words)
     const long long icg = LB ? uidx<D>(g, a - 1, j, p) : 0;
     T.inv_r = LB ? __ldg(Pr + 2 * g.vstride + icg) : pr0[2 * C::PROW + icn];
-    T.ut[2] = T.mt[2] = 0.0;
+    T.ut[2] = 0.0;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       T.ut[d] = LB ? __ldg(Pr + (3 + d) * g.vstride + icg) : pr0[(3 + d) * C::PROW + icn];
