@@ -87,6 +87,9 @@ struct UCfg {
 template <int D>
 __device__ __forceinline__ double phi_row(const DTransform& T, const double* X, int v) {
   // W_v = (Phi X)_v, constant part dropped (same formula as d_to_recon)
+#ifdef KFVM_ABL_NOPHI  // timing ablation (wrong results)
+  return X[v];
+#endif
   if (v == 0) return X[0];
   if (v <= D) return fma(-T.ut[v - 1], X[0], X[v]) * T.inv_r;
   double t = fma(T.ke, X[0], X[D + 1]);
@@ -306,14 +309,33 @@ __global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
 #pragma unroll
         for (int t = 0; t < NT; ++t)
 #pragma unroll
-          for (int v = 0; v < nv; ++v) tl[v][t] = fma(bt[t], aw[v], tl[v][t]);
+          for (int v = 0; v < nv; ++v) {
+#ifndef KFVM_ABL_NOTAIL  // timing ablation (wrong results): no tail derivative chains
+            tl[v][t] = fma(bt[t], aw[v], tl[v][t]);
+#endif
+          }
 #pragma unroll
         for (int u = 0; u < nv; ++u) av[u] = an[u];
 #pragma unroll
         for (int n = 0; n < NDM; ++n) bv[n] = bn[n];
 #pragma unroll
         for (int t = 0; t < NT; ++t) bt[t] = btn[t];
+#ifdef KFVM_ABL_NOBETA  // timing ablation (wrong results): no smoothness indicators
         if (sQ[ck] & 256) {
+          if (k4 == 0) {
+#pragma unroll
+            for (int v = 0; v < nv; ++v) sCw[(q * nv + v) * 8 + r8] = acc[v][0][0];
+          }
+#pragma unroll
+          for (int u = 0; u < nv; ++u)
+#pragma unroll
+            for (int n = 0; n < NDM; ++n) acc[u][n][0] = acc[u][n][1] = 0.0;
+          ++q;
+        }
+        if (false) {
+#else
+        if (sQ[ck] & 256) {
+#endif
           // acc[v][n][e]: variable v of cell r8, alpha = 8n + 2k4 + e; each
           // lane chains its own alphas (partial k4, (n, e) order) and the quad
           // combines (p0 + p1) + (p2 + p3) (oracle weno_field order; the xor
