@@ -976,8 +976,9 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
         (long long)((ch.ex - 2 * xsp + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
     constexpr bool LB = DIM == 3 && R == 2;
     if (LB) {
-      k_bounds<DIM><<<blocks(ext_range(ch), 256), 256, 0, h->stream>>>(U, h->Pr, h->Lb, h->g, ch,
-                                                                       h->d_err);
+      const long long nw = (long long)((ch.ex + 29) / 30) * ch.em * (ch.e1 - ch.e0);
+      k_bounds<3><<<(unsigned)((nw + 3) / 4), 128, 0, h->stream>>>(U, h->Pr, h->Lb, h->g, ch,
+                                                                  h->d_err);
       h->launches++;
     }
     k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(LB), h->stream>>>(

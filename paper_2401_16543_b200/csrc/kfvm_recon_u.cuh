@@ -759,45 +759,69 @@ __global__ void __launch_bounds__(128) k_limit_states(const double* __restrict__
 // k_states_u and k_limit_states): rho_max, rho_min, p_min into
 // Lb[3][extended cell], and the admissibility check of the average.  The
 // 3-D R=2 tensor engine reads them instead of keeping a ring of per-cell
-// quantities in shared memory.
-template <int D>
-__global__ void __launch_bounds__(256) k_bounds(const double* __restrict__ U,
-                                                const double* __restrict__ Pr,
-                                                double* __restrict__ Lb, Geo g, Chunk ch,
-                                                int* __restrict__ err) {
-  const long long tid = (long long)ch.e0 * ch.ex * ch.em + (long long)blockIdx.x * 256 + threadIdx.x;
-  if (tid >= (long long)ch.e1 * ch.ex * ch.em) return;
-  const int a = (int)(tid % ch.ex);
-  const long long r1 = tid / ch.ex;
-  const int b = (int)(r1 % ch.em), c = (int)(r1 / ch.em);
-  const int x = a - 1, j = D == 3 ? b - 1 : 0, p = ch.c0 - 1 + c;
-  const long long ic = uidx<D>(g, x, j, p);
-  const double rt = __ldg(U + ic), pt = __ldg(Pr + ic);
-  double rbmax = rt, rbmin = rt, pbmin = pt, cmin = __ldg(Pr + g.vstride + ic);
+// quantities in shared memory.  A warp takes 32 consecutive cells of one
+// row: each lane reduces its own column's 3 x 3 (mid, slab) neighbourhood,
+// the x neighbours' column results arrive by shuffles (min/max are exact,
+// so the reduction order is free); 3-D only.
+__device__ __forceinline__ void col_stats(const double* __restrict__ U,
+                                          const double* __restrict__ Pr, const Geo& g, int x,
+                                          int j, int p, double* st) {
+  st[0] = -INFINITY;  // rho max
+  st[1] = INFINITY;   // rho min
+  st[2] = INFINITY;   // p min
+  st[3] = INFINITY;   // c min
 #pragma unroll
   for (int cc = -1; cc <= 1; ++cc)
 #pragma unroll
-    for (int bb = (D == 3 ? -1 : 0); bb <= (D == 3 ? 1 : 0); ++bb)
+    for (int bb = -1; bb <= 1; ++bb) {
+      const long long o = uidx<3>(g, x, j + bb, p + cc);
+      const double r = __ldg(U + o);
+      st[0] = fmax(st[0], r);
+      st[1] = fmin(st[1], r);
+      st[2] = fmin(st[2], __ldg(Pr + o));
+      st[3] = fmin(st[3], __ldg(Pr + g.vstride + o));
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k_bounds(const double* __restrict__ U,
+                                                const double* __restrict__ Pr,
+                                                double* __restrict__ Lb, Geo g, Chunk ch,
+                                                int* __restrict__ err) {
+  static_assert(D == 3, "k_bounds serves the 3-D tensor engine");
+  // a warp covers 30 cells of a row: lane l reduces column a0 - 1 + l, lanes
+  // 1..30 own the cells (no divergent edge work)
+  const int lane = threadIdx.x & 31;
+  const long long wid = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int nseg = (ch.ex + 29) / 30;
+  const int seg = (int)(wid % nseg);
+  const long long r1 = wid / nseg;
+  const int b = (int)(r1 % ch.em);
+  const int c = ch.e0 + (int)(r1 / ch.em);
+  if (c >= ch.e1) return;  // whole warp
+  const int a = min(seg * 30 - 1 + lane, ch.ex);  // column of this lane (a = -1 .. ex)
+  const int x = a - 1, j = b - 1, p = ch.c0 - 1 + c;
+  double own[4], lft[4], rgt[4];
+  col_stats(U, Pr, g, x, j, p, own);
+  const double u0 = __ldg(Pr + 3 * g.vstride + uidx<3>(g, x, j, p));
 #pragma unroll
-      for (int aa = -1; aa <= 1; ++aa) {
-        const long long o = uidx<D>(g, x + aa, j + bb, p + cc);
-        const double r = __ldg(U + o);
-        rbmax = fmax(rbmax, r);
-        rbmin = fmin(rbmin, r);
-        pbmin = fmin(pbmin, __ldg(Pr + o));
-        cmin = fmin(cmin, __ldg(Pr + g.vstride + o));
-      }
-  double delta = 0.5 * (__ldg(Pr + 3 * g.vstride + uidx<D>(g, x + 1, j, p)) -
-                        __ldg(Pr + 3 * g.vstride + uidx<D>(g, x - 1, j, p)));
-  if (D == 3) {
-    delta = fma(0.5, __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j + 1, p)) -
-                         __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j - 1, p)), delta);
-    delta = fma(0.5, __ldg(Pr + 5 * g.vstride + uidx<D>(g, x, j, p + 1)) -
-                         __ldg(Pr + 5 * g.vstride + uidx<D>(g, x, j, p - 1)), delta);
-  } else {
-    delta = fma(0.5, __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j, p + 1)) -
-                         __ldg(Pr + 4 * g.vstride + uidx<D>(g, x, j, p - 1)), delta);
+  for (int k = 0; k < 4; ++k) {
+    lft[k] = __shfl_up_sync(0xffffffffu, own[k], 1);
+    rgt[k] = __shfl_down_sync(0xffffffffu, own[k], 1);
   }
+  const double ul = __shfl_up_sync(0xffffffffu, u0, 1), ur = __shfl_down_sync(0xffffffffu, u0, 1);
+  if (lane == 0 || lane == 31 || a < 0 || a >= ch.ex) return;
+  const long long ic = uidx<3>(g, x, j, p);
+  const double rt = __ldg(U + ic), pt = __ldg(Pr + ic);
+  const double rbmax = fmax(fmax(own[0], lft[0]), rgt[0]);
+  const double rbmin = fmin(fmin(own[1], lft[1]), rgt[1]);
+  const double pbmin = fmin(fmin(own[2], lft[2]), rgt[2]);
+  const double cmin = fmin(fmin(own[3], lft[3]), rgt[3]);
+  double delta = 0.5 * (ur - ul);
+  delta = fma(0.5, __ldg(Pr + 4 * g.vstride + uidx<3>(g, x, j + 1, p)) -
+                       __ldg(Pr + 4 * g.vstride + uidx<3>(g, x, j - 1, p)), delta);
+  delta = fma(0.5, __ldg(Pr + 5 * g.vstride + uidx<3>(g, x, j, p + 1)) -
+                       __ldg(Pr + 5 * g.vstride + uidx<3>(g, x, j, p - 1)), delta);
   const double kc = c_k.kf * cmin;
   double eta = -(delta + kc) / kc;
   eta = fmin(1.0, fmax(0.0, eta));
@@ -805,6 +829,7 @@ __global__ void __launch_bounds__(256) k_bounds(const double* __restrict__ U,
   const double flo = fma(-c_k.kappa, 1.0 - eta, 1.0);
   const double rmax = rbmax * fup, rmin = rbmin * flo, pmin = pbmin * flo;
   if (!(rt > 0.0) || !(pt > 0.0) || !(rmin > 0.0) || !(pmin > 0.0)) atomicOr(err, 2);
+  const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
   Lb[tid] = rmax;
   Lb[ch.next + tid] = rmin;
   Lb[2 * ch.next + tid] = pmin;
