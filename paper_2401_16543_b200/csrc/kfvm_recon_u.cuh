@@ -103,7 +103,7 @@ __device__ __forceinline__ double phi_row(const DTransform& T, const double* X, 
 // 0, raw conservative U as the A operand, the r_0 face vectors as B, the
 // unlimited states stored as they come out of the accumulators.
 template <int D, int R, bool P1 = false, bool KXM = false>
-__global__ void __launch_bounds__(128, UCfg<D, R>::MINB)
+__global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCfg<D, R>::MINB) : UCfg<D, R>::MINB)
     k_states_u(const double* __restrict__ U, const double* __restrict__ Pr,
                double* __restrict__ St, Geo g, Chunk ch, int KZ, int* __restrict__ err,
                const double* __restrict__ Bd, const double* __restrict__ Bf,
