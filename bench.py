@@ -381,11 +381,25 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    # large fields: the fields' steps are chained on the device (each waits
+    # for the previous field's step) so the SMs run one step at a time while
+    # the copy engines move the other fields — concurrent steps would share the
+    # SMs and finish together, leaving their copies exposed (config 4: e2e
+    # 3.54e8 -> 4.13e8).  Small fields keep the steps concurrent, which hides
+    # their launch gaps instead (config 2: 2.29e9 concurrent, 2.20e9 chained).
+    chain = nloc * 8 > (1 << 30)
+    streams = [torch.cuda.ExternalStream(sv.stream) for sv, _ in fields]
+    done = [torch.cuda.Event() for _ in fields]
     t0 = time.perf_counter()
+    prev = None
     for _ in range(e2e_steps):
-        for sv, hb in fields:
+        for i, (sv, hb) in enumerate(fields):
             sv.set_state_async(hb)
+            if chain and prev is not None:
+                streams[i].wait_event(done[prev])
             sv.run_async(1)
+            done[i].record(streams[i])
+            prev = i
             sv.get_state_async(hb)
     for sv, _ in fields:
         sv.sync()
@@ -437,7 +451,8 @@ def main():
                     "steps": e2e_steps,
                     "api": f"Solver.set_state_async/run_async/get_state_async (C-ABI), {nf} fields "
                            f"on {nf} handles: each field-step uploads from pinned host memory and "
-                           "reads back; the copy engines overlap the other fields' steps",
+                           "reads back; the copy engines overlap the other fields' steps" +
+                           (" (steps chained on the device by stream events)" if chain else ""),
                     "serial_value": e2e_serial,
                     "serial_api": "Solver.set_state/ssp_rk3_step/get_state, one field, no overlap"},
             "roofline": {"bound": "fp64", "kernel": "k_states_* (reconstruction+WENO-AO+limiter)",
