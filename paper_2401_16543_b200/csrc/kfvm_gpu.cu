@@ -2380,7 +2380,14 @@ int run_steps(kfvm_handle* h, int nsteps, bool reset) {
   }
   int rc = enqueue_speed(h);
   if (rc) return rc;
-  if (h->timing || h->loop) {  // loopback rendezvous is host-side: not capturable
+  // loopback rendezvous is host-side (not capturable); NCCL multi-rank steps
+  // are captured unless KFVM_NCCL_GRAPHS=0 (eager fallback for an NCCL build
+  // that cannot capture p2p)
+  static const bool nccl_graphs = [] {
+    const char* e = std::getenv("KFVM_NCCL_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  if (h->timing || h->loop || (h->multi && !nccl_graphs)) {
     for (int s = 0; s < nsteps; ++s)
       if ((rc = enqueue_step(h))) return rc;
     return KFVM_OK;
