@@ -11,6 +11,8 @@
 // plus the slab-axis halo fill (fill_ghost S:553-561 / NCCL send-recv) and the
 // device-resident dt.  The translation unit is compiled with -fmad=false:
 // every fma below is explicit, matching the oracle's FP contract.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -702,6 +704,8 @@ struct kfvm_handle {
   double* Pr = nullptr;  // k_prims output: p, c, 1/rho, u_d per cell (incl. halos)
   double *St = nullptr, *F = nullptr, *aos = nullptr;
   double* Lb = nullptr;  // 3-D R=2 tensor engine: limiter bounds [3][extended cell] (inside St)
+  CUtensorMap* d_tmap = nullptr;  // 3-D R=2: TMA maps of U0, Ua, Ub (ring-plane boxes)
+  int tma = 1;                    // option "tma": ring planes by TMA when the segments allow
   size_t st_elems = 0, f_elems = 0, aos_elems = 0;
   int chunk = 0;
   int ring_split = 1;  // option "ring_split": ring columns by k_states_fast
@@ -981,8 +985,12 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
                                                                   h->d_err);
       h->launches++;
     }
+    // ring planes by TMA: the ring-split segments start on an even x
+    const CUtensorMap* tm = nullptr;
+    if (LB && xsp && h->tma && h->d_tmap)
+      tm = U == h->U0 ? h->d_tmap : (U == h->Ua ? h->d_tmap + 1 : (U == h->Ub ? h->d_tmap + 2 : nullptr));
     k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(LB), h->stream>>>(
-        U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, nullptr, xsp, h->Lb);
+        U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, nullptr, xsp, h->Lb, tm);
     ring();
     dbg_sync(h, "k_states_u");
     if (UCfg<DIM, R>::NG > 1) {
@@ -1628,6 +1636,43 @@ int configure_scratch(kfvm_handle* h, long long chunk_planes) {
   return KFVM_OK;
 }
 
+// TMA tensor maps of the three state buffers for the tensor engine's ring
+// planes: 4-D (x, mid row, slab plane, variable) over the ghost-padded
+// storage, box = one region plane [var][2R+1 rows][32+2R columns].
+int make_tmaps(kfvm_handle* h) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!encode) {  // no driver entry point: the ring loads by cp.async
+    h->tma = 0;
+    return KFVM_OK;
+  }
+  using M = UCfg<3, 2>;
+  CUtensorMap maps[3];
+  double* bufs[3] = {h->U0, h->Ua, h->Ub};
+  const Geo& g = h->g;
+  cuuint64_t dims[4] = {(cuuint64_t)g.nxp, (cuuint64_t)(g.nm + 2 * g.Gm),
+                        (cuuint64_t)(g.np_loc + 2 * g.H), (cuuint64_t)h->nv};
+  cuuint64_t strides[3] = {(cuuint64_t)g.nxp * 8, (cuuint64_t)g.pstride * 8,
+                           (cuuint64_t)g.vstride * 8};
+  cuuint32_t box[4] = {(cuuint32_t)M::RX, (cuuint32_t)M::RY, 1, (cuuint32_t)h->nv};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  for (int i = 0; i < 3; ++i) {
+    CUresult r = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, bufs[i], dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(h, KFVM_ERR_DEVICE, "cuTensorMapEncodeTiled failed");
+  }
+  CK(cudaMalloc(&h->d_tmap, sizeof(maps)));
+  CK(cudaMemcpy(h->d_tmap, maps, sizeof(maps), cudaMemcpyHostToDevice));
+  return KFVM_OK;
+}
+
 // Upload the weights into the generated __constant__ arrays after checking
 // that the table's geometry is the structure compiled into kfvm_gen.cuh
 // (once per device: the registry's first handle).
@@ -2035,6 +2080,7 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
   bad(cudaMalloc(&h->Ua, ufull * sizeof(double)), "cudaMalloc Ua");
   bad(cudaMalloc(&h->Ub, ufull * sizeof(double)), "cudaMalloc Ub");
   bad(cudaMalloc(&h->Pr, (size_t)h->g.vstride * (cfg->dim + 3) * sizeof(double)), "cudaMalloc prims");
+  if (rc == KFVM_OK && cfg->dim == 3 && cfg->radius == 2) rc = make_tmaps(h);
   if (rc == KFVM_OK) {
     bad(cudaMemset(h->U0, 0, ufull * sizeof(double)), "memset");
     bad(cudaMemset(h->Ua, 0, ufull * sizeof(double)), "memset");
@@ -2139,7 +2185,7 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
       im = DeviceImage();
     }
   }
-  for (void* p : {(void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
+  for (void* p : {(void*)h->d_tmap, (void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
                   (void*)h->aos, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
                   (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_gat8, (void*)h->d_edges, (void*)h->d_tt,
@@ -2580,6 +2626,11 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
       h->engine = value ? 2 : 0;
     }
     return configure_scratch(h, 0);
+  }
+  if (n == "tma") {
+    drop_graphs(h);
+    h->tma = value ? 1 : 0;
+    return KFVM_OK;
   }
   if (n == "ring_split") {
     drop_graphs(h);

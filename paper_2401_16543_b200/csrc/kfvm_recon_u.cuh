@@ -79,7 +79,8 @@ struct UCfg {
   // LB: the instance whose limiter bounds come from k_bounds (3-D R=2 main
   // engine): no per-cell-quantity ring in shared memory
   static constexpr size_t bytes(bool lb = false) {
-    return sizeof(double) * (RING * PL + (lb ? 0 : PRING * PPL) + 4 * SCW + SB) +
+    return sizeof(double) * (RING * (lb ? (PL + 15) / 16 * 16 : PL) + (lb ? 0 : PRING * PPL) + 4 * SCW + SB) +
+           (lb ? sizeof(unsigned long long) * (RING + 1) : 0) +
            sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK + 4 * NCH2) + KFVM_U_EXTRA_SMEM;
   }
 };
@@ -108,21 +109,33 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
                double* __restrict__ St, Geo g, Chunk ch, int KZ, int* __restrict__ err,
                const double* __restrict__ Bd, const double* __restrict__ Bf,
                const int* __restrict__ gat4, const unsigned char* __restrict__ kfl = nullptr,
-               int xsp = 0, const double* __restrict__ Lb = nullptr) {
+               int xsp = 0, const double* __restrict__ Lb = nullptr,
+               const CUtensorMap* __restrict__ tmap = nullptr) {
   using G = Gen<D, R>;
   using C = UCfg<D, R>;
   // LB: per-cell limiter bounds {rho_max, rho_min, p_min} from k_bounds and
   // the transform's per-cell quantities from Pr in global memory (no ring)
   constexpr bool LB = D == 3 && R == 2 && !P1 && !KXM && C::NG == 1;
   constexpr int nv = C::nv, NP = G::NP, NS = G::NS, ND = C::ND, NPT = C::NPT;
-  extern __shared__ double smem[];
+  // LB with a tensor map (tmap): the U planes arrive by TMA — one elected
+  // thread, one 4-D box [var][row][x] per plane, an mbarrier per ring slot.
+  // FP64 boxes must start on an even x, which holds for the ring-split
+  // segments (x0 - R = 32 seg - 2); otherwise the host passes no map and the
+  // planes load by cp.async.
+  constexpr int RXk = C::RX;
+  constexpr int RROWk = C::RY * RXk, PLk = C::nv * RROWk;
+  // ring slot stride: TMA destinations are 128-byte aligned
+  constexpr int SLk = LB ? (PLk + 15) / 16 * 16 : PLk;
+  extern __shared__ __align__(128) double smem[];
   double* sRing = smem;                          // [RING][nv][RY][RX]
-  double* sPr = sRing + C::RING * C::PL;         // [PRING][NF][NY][NX]
+  double* sPr = sRing + C::RING * SLk;         // [PRING][NF][NY][NX]
   double* sC = sPr + (LB ? 0 : C::PRING * C::PPL);  // [warp][q][v][8]
   double* sBd = sC + 4 * C::SCW;                 // B fragments [chunk][n][lane]
   double* sBf = sBd + G::NCHUNK * ND * 32;
   int* sTab = reinterpret_cast<int*>(sBd + C::SB);  // [chunk][4] {inplane, oz}
   int* sQ = sTab + 8 * G::NCHUNK;                        // stencil | last << 8
+  unsigned long long* sBar = reinterpret_cast<unsigned long long*>(
+      sTab + ((9 * G::NCHUNK + 4 * C::NCH2 + 1) & ~1));   // LB: mbarrier per ring slot
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int k4 = lane & 3, r8 = lane >> 2;
@@ -152,7 +165,10 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   const int cidx = w + 4 * r8;
   const int a = xsp + seg * 32 + cidx;  // extended x index of this lane's cell
   const bool active = a < ch.ex - xsp;
-  const int xr = cidx + R;            // the cell's x in the region
+  const int sx = 0;
+  const bool use_tma = LB && tmap != nullptr;
+  const int xr = cidx + R + sx;       // the cell's x in the region
+  const int cb = cidx + sx;           // the cell's column offset in a ring row
   if constexpr (KXM) {  // KXRCF: a tile without a flagged cell has nothing to do
     bool any = false;
     for (int i = threadIdx.x; i < 32 * (cend - cstart); i += 128) {
@@ -164,10 +180,10 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
 
   // x indices (remapped) of the region columns this thread copies
   auto load_plane = [&](int p) {  // region plane p -> ring slot
-    double* dst = sRing + ((p + 4 * C::RING) % C::RING) * C::PL;
+    double* dst = sRing + ((p + 4 * C::RING) % C::RING) * SLk;
     const long long pbase = (long long)(p + g.H) * g.pstride;
-    for (int i = threadIdx.x; i < C::PL; i += 128) {
-      const int rx = i % C::RX, rr = i / C::RX;
+    for (int i = threadIdx.x; i < PLk; i += 128) {
+      const int rx = i % RXk, rr = i / RXk;
       const int ry = rr % C::RY, v = rr / C::RY;
       const int xx = xoff(g, x0 - R + rx);
       const long long off = v * g.vstride + pbase + xx +
@@ -187,13 +203,35 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
       __pipeline_memcpy_async(dst + i, Pr + off, sizeof(double));
     }
   };
+  // LB: TMA of region plane q into its ring slot (thread 0); plane q's slot
+  // completes its ((q - base) / RING)-th phase when the bytes have landed
+  const int base = ch.c0 - 1 + cstart - R;
+  auto tma_plane = [&](int q) {
+    const int sl = (q + 4 * C::RING) % C::RING;
+    mbar_expect_tx(&sBar[sl], (unsigned)(PLk * sizeof(double)));
+    tma_load_4d(sRing + sl * SLk, tmap, &sBar[sl], g.xo + x0 - R - sx, j - R + g.Gm, q + g.H, 0);
+  };
+  auto wait_plane = [&](int q) {
+    mbar_wait(&sBar[(q + 4 * C::RING) % C::RING], (unsigned)(((q - base) / C::RING) & 1));
+  };
   {
     const int p = ch.c0 - 1 + cstart;
-    for (int oz = -R; oz <= R; ++oz) load_plane(p + oz);
-    if (!P1 && !LB)  // pass 1 needs neither the transform nor the limiter statistics
-      for (int oz = -1; oz <= 1; ++oz) load_prims(p + oz);
-    __pipeline_commit();
-    __pipeline_wait_prior(0);
+    if (use_tma) {
+      if (threadIdx.x == 0) {
+        for (int sl = 0; sl < C::RING; ++sl) mbar_init(&sBar[sl], 1);
+        mbar_init_fence();
+      }
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int oz = -R; oz <= R; ++oz) tma_plane(p + oz);
+      for (int oz = -R; oz <= R; ++oz) wait_plane(p + oz);
+    } else {
+      for (int oz = -R; oz <= R; ++oz) load_plane(p + oz);
+      if (!P1 && !LB)  // pass 1 needs neither the transform nor the limiter statistics
+        for (int oz = -1; oz <= 1; ++oz) load_prims(p + oz);
+      __pipeline_commit();
+      __pipeline_wait_prior(0);
+    }
   }
   __syncthreads();
 
@@ -201,11 +239,16 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   PHASE_T0();
   for (int c = cstart; c < cend; ++c) {
     const int p = ch.c0 - 1 + c;
-    if (c + 1 < cend) {
-      load_plane(p + R + 1);
-      if (!P1 && !LB) load_prims(p + 2);
+    if (use_tma) {
+      if (threadIdx.x == 0 && c + 1 < cend) tma_plane(p + R + 1);
+      if (c > cstart) wait_plane(p + R);  // issued in the previous iteration
+    } else {
+      if (c + 1 < cend) {
+        load_plane(p + R + 1);
+        if (!P1 && !LB) load_prims(p + 2);
+      }
+      __pipeline_commit();
     }
-    __pipeline_commit();
     // KXRCF: the WENO passes run only for planes of this segment holding a
     // flagged cell; the limiter epilogue runs for every cell (unflagged cells
     // limit their pass-1 states from St)
@@ -222,13 +265,13 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     const int slot0 = (p - R + 4 * C::RING) % C::RING;  // slot of plane p - R
     auto plane = [&](int ozr) -> const double* {       // ozr = oz + R
       const int sl = slot0 + ozr;
-      return sRing + (sl >= C::RING ? sl - C::RING : sl) * C::PL;
+      return sRing + (sl >= C::RING ? sl - C::RING : sl) * SLk;
     };
     const double* pr0 = sPr + ((p + 4 * C::PRING) % C::PRING) * C::PPL;
     const double* prm = sPr + ((p - 1 + 4 * C::PRING) % C::PRING) * C::PPL;
     const double* prp = sPr + ((p + 1 + 4 * C::PRING) % C::PRING) * C::PPL;
     const int icn = (D == 3 ? C::NX : 0) + xr - R + 1;  // cell centre in a prims plane
-    const int icr = (D == 3 ? R * C::RX : 0) + xr;      // cell centre in a region plane
+    const int icr = (D == 3 ? R * RXk : 0) + xr;      // cell centre in a region plane
     // ---- transform of the cell average (identical to d_make_transform)
     DTransform T;
     // rho~ and m~ enter only Phi^-1 (after pass 2): with one point group they
@@ -238,7 +281,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
       T.rt = plane(R)[icr];
       T.mt[2] = 0.0;
 #pragma unroll
-      for (int d = 0; d < D; ++d) T.mt[d] = plane(R)[(1 + d) * C::RROW + icr];
+      for (int d = 0; d < D; ++d) T.mt[d] = plane(R)[(1 + d) * RROWk + icr];
     };
     if (!LATE_RM) load_rm();
     // LB: the cell's per-cell quantities straight from Pr (the quad's lanes
@@ -279,9 +322,9 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
       double av[nv], bv[NDM], bt[NTA];
       {
         const int inpl = sTab[2 * k4], oz = sTab[2 * k4 + 1];
-        const double* ap = plane(oz + R) + inpl + cidx;
+        const double* ap = plane(oz + R) + inpl + cb;
 #pragma unroll
-        for (int u = 0; u < nv; ++u) av[u] = ap[u * C::RROW];
+        for (int u = 0; u < nv; ++u) av[u] = ap[u * RROWk];
 #pragma unroll
         for (int n = 0; n < NDM; ++n) bv[n] = Bdp[n * 32 + lane];
 #pragma unroll
@@ -291,10 +334,10 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
       for (int ck = 0; ck < G::NCHUNK; ++ck) {
         const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
         const int inpl = sTab[2 * (cn * 4 + k4)], oz = sTab[2 * (cn * 4 + k4) + 1];
-        const double* ap = plane(oz + R) + inpl + cidx;
+        const double* ap = plane(oz + R) + inpl + cb;
         double an[nv], bn[NDM], btn[NTA];
 #pragma unroll
-        for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
+        for (int u = 0; u < nv; ++u) an[u] = ap[u * RROWk];
 #pragma unroll
         for (int n = 0; n < NDM; ++n) bn[n] = Bdp[(cn * ND + n) * 32 + lane];
 #pragma unroll
@@ -463,9 +506,9 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
       {
         int inpl, ozr;
         slot(0, inpl, ozr, qa);
-        const double* ap = plane(ozr) + inpl + cidx;
+        const double* ap = plane(ozr) + inpl + cb;
 #pragma unroll
-        for (int u = 0; u < nv; ++u) av[u] = ap[u * C::RROW];
+        for (int u = 0; u < nv; ++u) av[u] = ap[u * RROWk];
 #pragma unroll
         for (int n = 0; n < PG; ++n) bv[n] = t0 + n < NPT ? bfrag(0, t0 + n) : 0.0;
       }
@@ -474,10 +517,10 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
         const int cn = ck + 1 < NCK ? ck + 1 : ck;
         int inpl, ozr, qn;
         slot(cn, inpl, ozr, qn);
-        const double* ap = plane(ozr) + inpl + cidx;
+        const double* ap = plane(ozr) + inpl + cb;
         double an[nv], bn[PG];
 #pragma unroll
-        for (int u = 0; u < nv; ++u) an[u] = ap[u * C::RROW];
+        for (int u = 0; u < nv; ++u) an[u] = ap[u * RROWk];
 #pragma unroll
         for (int n = 0; n < PG; ++n) bn[n] = t0 + n < NPT ? bfrag(cn, t0 + n) : 0.0;
         if (PK && qa != qcur) {  // this slot starts a new stencil
@@ -568,7 +611,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
           const int aa = m % 3 - 1;
           const int bb = D == 3 ? (m / 3) % 3 - 1 : 0;
           const int cc = D == 3 ? m / 9 - 1 : m / 3 - 1;
-          const double r = plane(R + cc)[(D == 3 ? bb * C::RX : 0) + icr + aa];
+          const double r = plane(R + cc)[(D == 3 ? bb * RXk : 0) + icr + aa];
           const double* prz = cc < 0 ? prm : (cc > 0 ? prp : pr0);
           const int ip = (D == 3 ? bb * C::NX : 0) + icn + aa;
           rbmax = fmax(rbmax, r);
@@ -608,7 +651,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     Ubar[0] = rt;
 #pragma unroll
     for (int d = 0; d < D; ++d) Ubar[1 + d] = T.mt[d];
-    Ubar[nv - 1] = plane(R)[(nv - 1) * C::RROW + icr];
+    Ubar[nv - 1] = plane(R)[(nv - 1) * RROWk + icr];
     double th = 1.0;
 #pragma unroll
     for (int n = 0; n < NPT; ++n)

@@ -237,3 +237,25 @@ def test_async_two_handles_pipeline(require_gpu):
         b.sync()
     assert np.array_equal(bufs[0], ref2) and np.array_equal(bufs[1], ref2)
     assert not np.array_equal(ref1, ref2)
+
+
+@pytest.mark.parametrize("idx", [3, 4])
+def test_tma_ring_bitwise(require_gpu, idx):
+    """3-D R=2 with nx = 64 (ring split): the tensor engine's ring planes
+    arrive by TMA (cp.async.bulk.tensor + mbarrier); with option tma=0 by
+    cp.async.  Both, in one chunk and in several (chunk_planes), give the
+    oracle's bits."""
+    from dataclasses import replace
+    w = K.baseline_config(idx, n=8)
+    g = replace(w.grid, nx=64, ny=12, nz=14, dx=1.0 / 64)
+    U = K.initial_condition(g, w.ic)
+    rset = K.precompute(2, dim=3)
+    Uo, do = Oracle(g, rset).run(U, 2)
+    for opts in ((("tma", 1),), (("tma", 0),), (("tma", 1), ("chunk_planes", 4))):
+        with K.Solver(g, rset) as s:
+            for k, v in opts:
+                s.set_option(k, v)
+            s.set_state(U)
+            d = s.advance(2)
+            assert np.array_equal(d, do), opts
+            assert np.array_equal(s.get_state(), Uo), opts
