@@ -72,7 +72,7 @@ struct UCfg {
   static constexpr int MINB = D == 3 ? (R == 2 ? KFVM_U_MINB32 : KFVM_U_MINB) : 4;
   static constexpr int SB = BSMEM ? G::NCHUNK * (ND + NPT) * 32 : 0;  // B fragments
   // 3-D: pass 2 over chunks packed across stencil boundaries
-  static constexpr bool PK = D == 3;
+  static constexpr bool PK = D == 3 && R == 2;  // R=3 (point groups) measured slower packed
   static constexpr int NCH2 = PK ? (G::NTOT + 3) / 4 : 0;
   static constexpr int PG = NPT <= 3 ? NPT : 4;         // point tiles per pass-2 group
   static constexpr int NG = (NPT + PG - 1) / PG;         // groups (>1: limiter separate)
