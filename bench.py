@@ -253,6 +253,10 @@ def main():
     args = ap.parse_args()
 
     import paper_2401_16543_b200 as K
+    if args.config == 5 and args.nz is None and args.n is None:
+        # config 5's 1024^3 is an 8-GPU workload (180 GB per GPU do not hold
+        # it): its weak-scaling series, 1024 x 1024 x 128 per GPU (BASELINE.json)
+        args.nz = 128 * max(1, int(os.environ.get("WORLD_SIZE", args.gpus)))
     w = K.baseline_config(args.config, n=args.n, nz=args.nz)
     if args.kxrcf:
         from dataclasses import replace as _replace

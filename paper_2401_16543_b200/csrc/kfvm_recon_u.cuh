@@ -236,6 +236,21 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   __syncthreads();
 
   double* sCw = sC + w * C::SCW;
+  // LB: the transform's per-cell quantities (1/rho, u_d) of the warp's 8
+  // cells for plane q, staged in the warp's weight area sCw[f][cell] (free
+  // from the end of pass 2 until the next plane's transform is read)
+  auto load_t = [&](int q) {
+    const int f = lane >> 3, cc = w + 4 * (lane & 7);
+    const int ac = min(xsp + seg * 32 + cc, ch.ex - 1);
+    __pipeline_memcpy_async(sCw + f * 8 + (lane & 7),
+                            Pr + (2 + f) * g.vstride + uidx<D>(g, ac - 1, j, q), sizeof(double));
+  };
+  if constexpr (LB) {
+    load_t(ch.c0 - 1 + cstart);
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
+    __syncwarp();
+  }
   PHASE_T0();
   for (int c = cstart; c < cend; ++c) {
     const int p = ch.c0 - 1 + c;
@@ -286,13 +301,11 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     if (!LATE_RM) load_rm();
     // LB: the cell's per-cell quantities straight from Pr (the quad's lanes
     // load the same words)
-    const long long icg = LB ? uidx<D>(g, a - 1, j, p) : 0;
-    T.inv_r = LB ? __ldg(Pr + 2 * g.vstride + icg) : pr0[2 * C::PROW + icn];
+    T.inv_r = LB ? sCw[r8] : pr0[2 * C::PROW + icn];
     T.ut[2] = 0.0;
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      T.ut[d] = LB ? __ldg(Pr + (3 + d) * g.vstride + icg) : pr0[(3 + d) * C::PROW + icn];
-    }
+    for (int d = 0; d < D; ++d) T.ut[d] = LB ? sCw[(1 + d) * 8 + r8] : pr0[(3 + d) * C::PROW + icn];
+    if (LB) __syncwarp();  // every lane has its transform before pass 1 reuses sCw
     {
       double ke = T.ut[0] * T.ut[0];
       ke = fma(T.ut[1], T.ut[1], ke);
@@ -581,6 +594,11 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     }
     }
     PHASE_MARK(3);
+    if constexpr (LB) {  // the next plane's transform quantities, hidden by the epilogue
+      __syncwarp();
+      if (c + 1 < cend) load_t(p + 1);
+      __pipeline_commit();
+    }
     if constexpr (NG == 1 && !P1 && !KXM) {
     {
     if (LATE_RM) load_rm();
