@@ -887,6 +887,24 @@ void dbg_sync(kfvm_handle* h, const char* what) {
   if (e != cudaSuccess) fprintf(stderr, "[kfvm] %s: %s\n", what, cudaGetErrorString(e));
 }
 
+// Periodic x: the extended box's two ring columns are periodic images of
+// the interior columns x = nx-1 and x = 0 (their stencil neighbourhoods,
+// ghost cells included, hold the same values), so their face states are the
+// images' face states, copied instead of recomputed (bit-identical).
+__global__ void k_ring_copy(double* __restrict__ St, Chunk ch, int nkv) {
+  const long long n = 2LL * ch.em * (ch.e1 - ch.e0);
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * nkv) return;
+  const int k = (int)(t / n);
+  const long long r = t % n;
+  const int side = (int)(r & 1);
+  const long long rb = r >> 1;  // (plane, row)
+  const int b = (int)(rb % ch.em), c = ch.e0 + (int)(rb / ch.em);
+  const long long row = ((long long)c * ch.em + b) * ch.ex;
+  const long long dst = row + (side ? ch.ex - 1 : 0), src = row + (side ? 1 : ch.ex - 2);
+  St[(long long)k * ch.next + dst] = St[(long long)k * ch.next + src];
+}
+
 template <int DIM, int R>
 void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   tic(h);
@@ -951,10 +969,19 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
   // contract)
   // (3-D only: in 2-D the ring columns are ~2k cells, a 65-CTA launch whose
   // latency (13 us) exceeds the saved segment (10 us), measured config 2)
-  const int xsp = (DIM == 3 && Gen<DIM, R>::UNROLLED && h->ring_split &&
-                   (ch.ex - 2 + 31) / 32 < (ch.ex + 31) / 32) ? 1 : 0;
+  // periodic x (engine 2): the ring columns are copies of their periodic
+  // images (k_ring_copy), so the segments always cover interior x only
+  const bool ringcopy = DIM == 3 && h->engine == 2 && h->kc.per[0] != 0 && h->ring_split;
+  const int xsp = (ringcopy || (DIM == 3 && Gen<DIM, R>::UNROLLED && h->ring_split &&
+                                (ch.ex - 2 + 31) / 32 < (ch.ex + 31) / 32)) ? 1 : 0;
   auto ring = [&]() {
     if (!xsp) return;
+    if (ringcopy) {
+      const long long n = 2LL * ch.em * (ch.e1 - ch.e0) * h->NP * h->nv;
+      k_ring_copy<<<blocks(n, 256), 256, 0, h->stream>>>(h->St, ch, h->NP * h->nv);
+      h->launches++;
+      return;
+    }
     const long long nr = 2LL * ch.em * (ch.e1 - ch.e0);
     if constexpr (Gen<DIM, R>::UNROLLED)
       k_states_fast<DIM, R, true><<<(unsigned)((nr + 31) / 32), 32 * (DIM + 2), 0, h->stream>>>(
@@ -993,7 +1020,7 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
         U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, nullptr, xsp, h->Lb, tm);
     ring();
     dbg_sync(h, "k_states_u");
-    if (UCfg<DIM, R>::NG > 1) {
+    if (UCfg<DIM, R>::NG > 1) {  // (the ring copies above precede the limiter)
       h->launches++;
       k_limit_states<DIM, R><<<blocks(ext_range(ch), 128), 128, 0, h->stream>>>(U, h->Pr, h->St, h->g, ch,
                                                                           h->d_err);

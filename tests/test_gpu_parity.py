@@ -259,3 +259,22 @@ def test_tma_ring_bitwise(require_gpu, idx):
             d = s.advance(2)
             assert np.array_equal(d, do), opts
             assert np.array_equal(s.get_state(), Uo), opts
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_periodic_ring_copy_bitwise(require_gpu, R):
+    """Periodic x: the extended box's ring columns are copied from their
+    periodic images (k_ring_copy) instead of recomputed; with the option
+    ring_split=0 every column is computed.  Both equal the oracle."""
+    from dataclasses import replace
+    w = K.baseline_config(3 if R == 2 else 5, n=8)
+    g = replace(w.grid, nx=32, ny=9, nz=10, dx=1.0 / 32)
+    U = K.initial_condition(g, w.ic)
+    rset = K.precompute(R, dim=3)
+    Uo, do = Oracle(g, rset).run(U, 2)
+    for split in (1, 0):
+        with K.Solver(g, rset) as s:
+            s.set_option("ring_split", split)
+            s.set_state(U)
+            d = s.advance(2)
+            assert np.array_equal(d, do) and np.array_equal(s.get_state(), Uo), split
