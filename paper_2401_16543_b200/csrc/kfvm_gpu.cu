@@ -706,6 +706,7 @@ struct kfvm_handle {
   double* Lb = nullptr;  // 3-D R=2 tensor engine: limiter bounds [3][extended cell] (inside St)
   CUtensorMap* d_tmap = nullptr;  // 3-D R=2: TMA maps of U0, Ua, Ub (ring-plane boxes)
   int tma = 1;                    // option "tma": ring planes by TMA when the segments allow
+  int ring_tiles = 1;             // option "ring_tiles": ring columns on the tensor engine
   size_t st_elems = 0, f_elems = 0, aos_elems = 0;
   int chunk = 0;
   int ring_split = 1;  // option "ring_split": ring columns by k_states_fast
@@ -731,6 +732,7 @@ struct kfvm_handle {
   bool grav = false;  // gravity source in k_update
   double *d_Bd = nullptr, *d_Bf = nullptr;
   int* d_gat4 = nullptr;
+  int* d_gat4c = nullptr;   // 3-D R=2: the chunk tables for the ring-column tiles ([36 rows][5 cols])
   int* d_gat8 = nullptr;    // chunk tables of the fused 3-D engine's 8x4 tile
   double* d_edges = nullptr;  // tile-edge face states of the fused 3-D engine
   size_t edge_elems = 0;
@@ -981,6 +983,19 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
       k_ring_copy<<<blocks(n, 256), 256, 0, h->stream>>>(h->St, ch, h->NP * h->nv);
       h->launches++;
       return;
+    }
+    if constexpr (DIM == 3 && R == 2) {
+      if (h->engine == 2 && h->d_gat4c && h->ring_tiles) {  // ring columns on the tensor engine
+        // few tiles (2 columns x mid/32): short z blocks for enough CTAs
+        const int KZ = h->ring_tiles > 1 ? h->ring_tiles : 4;
+        const long long nb = 2LL * ((ch.em + 31) / 32) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
+        k_states_u<3, 2, false, false, true><<<(unsigned)nb, 128, UCfg<3, 2>::bytes(true),
+                                                 h->stream>>>(
+            U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4c, nullptr, 1,
+            h->Lb, nullptr);
+        h->launches++;
+        return;
+      }
     }
     const long long nr = 2LL * ch.em * (ch.e1 - ch.e0);
     if constexpr (Gen<DIM, R>::UNROLLED)
@@ -1821,6 +1836,25 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
       CK(cudaFuncSetAttribute(k_fused3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)FCfg<2>::bytes()));
   }
+  if constexpr (D == 3 && R == 2) {
+    // the same slots in the ring-column tile's layout [36 rows][5 columns]:
+    // region offset (oy + R) * 5 + ox + R
+    std::vector<int> gc(g4);
+    constexpr int CX = 2 * R + 1;
+    auto col_inpl = [&](int inpl_row) {  // row-tile offset (oy + R) * RX + ox + R -> column tile
+      const int oyr = inpl_row / M::RX, oxr = inpl_row % M::RX;
+      return oyr * CX + oxr;
+    };
+    for (int ck = 0; ck < G::NCHUNK; ++ck)
+      for (int k = 0; k < 4; ++k) gc[(size_t)(ck * 4 + k) * 2] = col_inpl(g4[(size_t)(ck * 4 + k) * 2]);
+    const size_t g0 = (size_t)G::NCHUNK * 9;
+    for (size_t i = g0; i < gc.size(); ++i) {
+      const int w = g4[i];
+      gc[i] = col_inpl(w & 511) | (w & ~511);
+    }
+    CK(cudaMalloc(&h->d_gat4c, gc.size() * sizeof(int)));
+    CK(cudaMemcpy(h->d_gat4c, gc.data(), gc.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
   CK(cudaMalloc(&h->d_Bd, bd.size() * sizeof(double)));
   CK(cudaMalloc(&h->d_Bf, bf.size() * sizeof(double)));
   CK(cudaMalloc(&h->d_gat4, g4.size() * sizeof(int)));
@@ -1829,6 +1863,9 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   CK(cudaMemcpy(h->d_gat4, g4.data(), g4.size() * sizeof(int), cudaMemcpyHostToDevice));
   CK(cudaFuncSetAttribute(k_states_u<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)M::bytes(D == 3 && R == 2)));
+  if constexpr (D == 3 && R == 2)
+    CK(cudaFuncSetAttribute(k_states_u<D, R, false, false, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M::bytes(true)));
   CK(cudaFuncSetAttribute(k_states_u<D, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)M::bytes()));
   CK(cudaFuncSetAttribute(k_states_u<D, R, false, true>,
@@ -2212,7 +2249,7 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
       im = DeviceImage();
     }
   }
-  for (void* p : {(void*)h->d_tmap, (void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
+  for (void* p : {(void*)h->d_gat4c, (void*)h->d_tmap, (void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
                   (void*)h->aos, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
                   (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_gat8, (void*)h->d_edges, (void*)h->d_tt,
@@ -2653,6 +2690,11 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
       h->engine = value ? 2 : 0;
     }
     return configure_scratch(h, 0);
+  }
+  if (n == "ring_tiles") {
+    drop_graphs(h);
+    h->ring_tiles = value < 0 ? 0 : (int)value;  // 0 off, 1 on (KZ 4), > 1: its KZ
+    return KFVM_OK;
   }
   if (n == "tma") {
     drop_graphs(h);

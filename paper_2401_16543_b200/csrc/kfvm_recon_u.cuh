@@ -103,7 +103,7 @@ __device__ __forceinline__ double phi_row(const DTransform& T, const double* X, 
 // P1: KXRCF pass 1 on the tensor cores — only the chunks of stencil
 // 0, raw conservative U as the A operand, the r_0 face vectors as B, the
 // unlimited states stored as they come out of the accumulators.
-template <int D, int R, bool P1 = false, bool KXM = false>
+template <int D, int R, bool P1 = false, bool KXM = false, bool COL = false>
 __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCfg<D, R>::MINB) : UCfg<D, R>::MINB)
     k_states_u(const double* __restrict__ U, const double* __restrict__ Pr,
                double* __restrict__ St, Geo g, Chunk ch, int KZ, int* __restrict__ err,
@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   // LB: per-cell limiter bounds {rho_max, rho_min, p_min} from k_bounds and
   // the transform's per-cell quantities from Pr in global memory (no ring)
   constexpr bool LB = D == 3 && R == 2 && !P1 && !KXM && C::NG == 1;
+  constexpr bool col = COL && LB;  // ring-column tile instance
   constexpr int nv = C::nv, NP = G::NP, NS = G::NS, ND = C::ND, NPT = C::NPT;
   // LB with a tensor map (tmap): the U planes arrive by TMA — one elected
   // thread, one 4-D box [var][row][x] per plane, an mbarrier per ring slot.
@@ -149,26 +150,44 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   const double* Bfp = C::BSMEM ? sBf : Bf;
 
   // xsp = 1: the segments cover the interior x range only (the two ring
-  // columns of the extended box are computed by k_states_fast<.., true>)
-  const int nseg = (ch.ex - 2 * xsp + 31) >> 5;
+  // columns of the extended box are computed by column tiles (col = 1, the
+  // LB instance), copied from their periodic images, or by k_states_fast)
+  // col = 1 (LB): a CTA takes 32 cells of one ring column (x = -1 or nx)
+  // along the mid axis — the row tile transposed: the region plane is
+  // [var][36 rows][5 columns] (the same size), the host passes the chunk
+  // tables built for that layout, and the planes load by cp.async.
   int bid = blockIdx.x;
-  const int seg = bid % nseg;
-  bid /= nseg;
-  const int b = bid % ch.em;          // extended mid index
-  const int zblk = bid / ch.em;
+  int seg = 0, zblk, b, j0, a, cidx = w + 4 * r8;
+  if (LB && col) {
+    const int nys = (ch.em + 31) >> 5;
+    const int side = bid & 1;
+    bid >>= 1;
+    seg = bid % nys;  // y segment
+    zblk = bid / nys;
+    a = side ? ch.ex - 1 : 0;
+    b = seg * 32 + cidx;
+    j0 = seg * 32 - 1;  // mid index of the tile's first cell
+  } else {
+    const int nseg = (ch.ex - 2 * xsp + 31) >> 5;
+    seg = bid % nseg;
+    bid /= nseg;
+    b = bid % ch.em;  // extended mid index
+    zblk = bid / ch.em;
+    j0 = D == 3 ? b - 1 : 0;
+    a = xsp + seg * 32 + cidx;  // extended x index of this lane's cell
+  }
   const int cstart = ch.e0 + zblk * KZ, cend = min(ch.e1, cstart + KZ);
-  const int j = D == 3 ? b - 1 : 0;
-  const int x0 = xsp + seg * 32 - 1;  // x of the segment's first cell
+  const int j = (LB && col) ? b - 1 : j0;  // this lane's cell's mid index
+  // region origin: x of column 0 (+R) and mid index of row 0 (+R)
+  const int x0 = (LB && col) ? a - 1 : xsp + seg * 32 - 1;
   // warp w owns the cells w, w+4, ..., w+28 of the segment (stride 4): the 4
   // slots of a DMMA chunk are mostly consecutive x offsets, and with stride-4
   // rows the 16 (cell, slot) words of a half-warp fall in distinct banks
-  const int cidx = w + 4 * r8;
-  const int a = xsp + seg * 32 + cidx;  // extended x index of this lane's cell
-  const bool active = a < ch.ex - xsp;
+  const bool active = (LB && col) ? b < ch.em : a < ch.ex - xsp;
   const int sx = 0;
-  const bool use_tma = LB && tmap != nullptr;
-  const int xr = cidx + R + sx;       // the cell's x in the region
-  const int cb = cidx + sx;           // the cell's column offset in a ring row
+  const bool use_tma = LB && tmap != nullptr && !col;
+  const int xr = cidx + R + sx;       // the cell's x in the region (row tiles)
+  const int cb = (LB && col) ? cidx * (2 * R + 1) : cidx + sx;  // the cell's offset in a region plane
   if constexpr (KXM) {  // KXRCF: a tile without a flagged cell has nothing to do
     bool any = false;
     for (int i = threadIdx.x; i < 32 * (cend - cstart); i += 128) {
@@ -182,6 +201,17 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   auto load_plane = [&](int p) {  // region plane p -> ring slot
     double* dst = sRing + ((p + 4 * C::RING) % C::RING) * SLk;
     const long long pbase = (long long)(p + g.H) * g.pstride;
+    if (LB && col) {  // [var][36 rows][5 columns]
+      constexpr int CX = 2 * R + 1, CY = 32 + 2 * R;
+      for (int i = threadIdx.x; i < C::nv * CX * CY; i += 128) {
+        const int rx = i % CX, rr = i / CX;
+        const int ry = rr % CY, v = rr / CY;
+        const long long off =
+            v * g.vstride + pbase + xoff(g, x0 - R + rx) + moff(g, min(j0 - R + ry, g.nm + g.Gm - 1));
+        __pipeline_memcpy_async(dst + i, U + off, sizeof(double));
+      }
+      return;
+    }
     for (int i = threadIdx.x; i < PLk; i += 128) {
       const int rx = i % RXk, rr = i / RXk;
       const int ry = rr % C::RY, v = rr / C::RY;
@@ -241,9 +271,10 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   // from the end of pass 2 until the next plane's transform is read)
   auto load_t = [&](int q) {
     const int f = lane >> 3, cc = w + 4 * (lane & 7);
-    const int ac = min(xsp + seg * 32 + cc, ch.ex - 1);
+    const int ac = (LB && col) ? a : min(xsp + seg * 32 + cc, ch.ex - 1);
+    const int jc = (LB && col) ? min(seg * 32 + cc, ch.em - 1) - 1 : j;
     __pipeline_memcpy_async(sCw + f * 8 + (lane & 7),
-                            Pr + (2 + f) * g.vstride + uidx<D>(g, ac - 1, j, q), sizeof(double));
+                            Pr + (2 + f) * g.vstride + uidx<D>(g, ac - 1, jc, q), sizeof(double));
   };
   if constexpr (LB) {
     load_t(ch.c0 - 1 + cstart);
@@ -286,7 +317,8 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     const double* prm = sPr + ((p - 1 + 4 * C::PRING) % C::PRING) * C::PPL;
     const double* prp = sPr + ((p + 1 + 4 * C::PRING) % C::PRING) * C::PPL;
     const int icn = (D == 3 ? C::NX : 0) + xr - R + 1;  // cell centre in a prims plane
-    const int icr = (D == 3 ? R * RXk : 0) + xr;      // cell centre in a region plane
+    // cell centre in a region plane
+    const int icr = (LB && col) ? (cidx + R) * (2 * R + 1) + R : (D == 3 ? R * RXk : 0) + xr;
     // ---- transform of the cell average (identical to d_make_transform)
     DTransform T;
     // rho~ and m~ enter only Phi^-1 (after pass 2): with one point group they

@@ -278,3 +278,24 @@ def test_periodic_ring_copy_bitwise(require_gpu, R):
             s.set_state(U)
             d = s.advance(2)
             assert np.array_equal(d, do) and np.array_equal(s.get_state(), Uo), split
+
+
+@pytest.mark.parametrize("bc", ["outflow", "reflecting"])
+def test_ring_column_tiles_bitwise(require_gpu, bc):
+    """Non-periodic x with nx = 32 (ring split): the extended box's two ring
+    columns run on the tensor engine as transposed column tiles (32 cells
+    along the mid axis, region [36 rows][5 columns]); with the option
+    ring_tiles=0 the DFMA ring engine computes them.  Both give the oracle's
+    bits, including a mid extent that leaves a partial last column tile."""
+    from dataclasses import replace
+    w = K.baseline_config(4, n=8)
+    g = replace(w.grid, nx=32, ny=37, nz=9, dx=1.0 / 32, bc=bc)
+    U = K.initial_condition(g, w.ic)
+    rset = K.precompute(2, dim=3)
+    Uo, do = Oracle(g, rset).run(U, 2)
+    for tiles in (1, 0):
+        with K.Solver(g, rset) as s:
+            s.set_option("ring_tiles", tiles)
+            s.set_state(U)
+            d = s.advance(2)
+            assert np.array_equal(d, do) and np.array_equal(s.get_state(), Uo), tiles
