@@ -44,7 +44,7 @@ def test_3d_tensor_engine_fits_four_ctas_per_sm():
     """3-D R=2 tensor engine: 128 registers (4 x 128 threads per SM) with the
     documented small spill (kfvm_recon_u.cuh, KFVM_U_MINB32)."""
     ks = kernels()
-    for k, (regs, st, ld) in pick(ks, re.escape("k_states_u<3, 2, false, false>")).items():
+    for k, (regs, st, ld) in pick(ks, re.escape("k_states_u<3, 2, false, false, ")).items():
         assert regs <= 128 and st <= 64 and ld <= 64, (k, regs, st, ld)
 
 
