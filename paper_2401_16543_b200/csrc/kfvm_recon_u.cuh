@@ -80,7 +80,7 @@ struct UCfg {
   // engine): no per-cell-quantity ring in shared memory
   static constexpr size_t bytes(bool lb = false) {
     return sizeof(double) * (RING * (lb ? (PL + 15) / 16 * 16 : PL) + (lb ? 0 : PRING * PPL) + 4 * SCW + SB) +
-           (lb ? sizeof(unsigned long long) * (RING + 1) : 0) +
+           (lb ? sizeof(unsigned long long) * (RING + 3) : 0) +
            sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK + 4 * NCH2) + KFVM_U_EXTRA_SMEM;
   }
 };
@@ -137,6 +137,13 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   int* sQ = sTab + 8 * G::NCHUNK;                        // stencil | last << 8
   unsigned long long* sBar = reinterpret_cast<unsigned long long*>(
       sTab + ((9 * G::NCHUNK + 4 * C::NCH2 + 1) & ~1));   // LB: mbarrier per ring slot
+  // TMA path: no CTA barrier per plane.  A warp arrives on sDone[it & 1] after
+  // pass 2 of its it-th plane (its last read of the oldest ring plane); the
+  // issuing thread waits for the four arrivals of plane it - 1 before the TMA
+  // that overwrites that slot.  A warp can enter plane it only after every
+  // warp arrived for it - 2 (the plane it waits for was issued behind that
+  // wait), so two alternating barriers never mix phases.
+  unsigned long long* sDone = sBar + C::RING;
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int k4 = lane & 3, r8 = lane >> 2;
@@ -249,6 +256,8 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     if (use_tma) {
       if (threadIdx.x == 0) {
         for (int sl = 0; sl < C::RING; ++sl) mbar_init(&sBar[sl], 1);
+        mbar_init(&sDone[0], 4);
+        mbar_init(&sDone[1], 4);
         mbar_init_fence();
       }
       __syncthreads();
@@ -285,8 +294,11 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   PHASE_T0();
   for (int c = cstart; c < cend; ++c) {
     const int p = ch.c0 - 1 + c;
+    const int it = c - cstart;
     if (use_tma) {
+#ifdef KFVM_U_CTASYNC
       if (threadIdx.x == 0 && c + 1 < cend) tma_plane(p + R + 1);
+#endif
       if (c > cstart) wait_plane(p + R);  // issued in the previous iteration
     } else {
       if (c + 1 < cend) {
@@ -479,6 +491,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     // and normalises variable v = k4 (+4) — the same operations as one
     // sequential pass per variable
     if (!P1) {
+#ifdef KFVM_OMEGA_SEQ  // the plain divisions, one after the other (A/B timing)
 #pragma unroll
       for (int q = k4; q < NS; q += 4)
 #pragma unroll
@@ -501,9 +514,68 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
         for (int q = 1; q < NS; ++q)
           sCw[(q * nv + v) * 8 + r8] = fma(-c0, c_t.gamma_lin[q], wt[q] * inv_sum);
       }
+#else
+      // the lane's reciprocals as ONE interleaved batch (rcp_batch: the same
+      // bits as 1.0 / x; consecutive plain divisions run as serial chains)
+      constexpr int NQ = (NS + 3) / 4, NVL = (nv + 3) / 4;
+      {
+        double xs[NQ * nv], ys[NQ * nv];
+#pragma unroll
+        for (int i = 0; i < NQ; ++i)
+#pragma unroll
+          for (int v = 0; v < nv; ++v) {
+            const int q = k4 + 4 * i;
+            const double bb = q < NS ? sCw[(q * nv + v) * 8 + r8] : 1.0;
+            xs[i * nv + v] = fma(bb, bb, c_k.eps);
+          }
+        rcp_batch<NQ * nv>(xs, ys);
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) {
+          const int q = k4 + 4 * i;
+          if (q < NS) {
+            const double gq = c_t.gamma_lin[q];
+#pragma unroll
+            for (int v = 0; v < nv; ++v) sCw[(q * nv + v) * 8 + r8] = gq * ys[i * nv + v];
+          }
+        }
+      }
+      __syncwarp();
+      {
+        double wt[NVL][NS], sum[NVL], inv_sum[NVL];
+#pragma unroll
+        for (int i = 0; i < NVL; ++i) {
+          const int v = k4 + 4 * i;
+#pragma unroll
+          for (int q = 0; q < NS; ++q) wt[i][q] = v < nv ? sCw[(q * nv + v) * 8 + r8] : 1.0;
+          sum[i] = wt[i][0];
+#pragma unroll
+          for (int q = 1; q < NS; ++q) sum[i] = sum[i] + wt[i][q];
+        }
+        rcp_batch<NVL>(sum, inv_sum);
+#pragma unroll
+        for (int i = 0; i < NVL; ++i) {
+          const int v = k4 + 4 * i;
+          if (v < nv) {
+            const double c0 = (wt[i][0] * inv_sum[i]) * c_t.inv_g0;
+            sCw[v * 8 + r8] = c0;
+#pragma unroll
+            for (int q = 1; q < NS; ++q)
+              sCw[(q * nv + v) * 8 + r8] = fma(-c0, c_t.gamma_lin[q], wt[i][q] * inv_sum[i]);
+          }
+        }
+      }
+#endif
     }
     __syncwarp();
     PHASE_MARK(2);
+#ifndef KFVM_U_CTASYNC
+    // the next plane's TMA, issued here (half a plane before it is needed)
+    // so that the wait for the other warps' arrivals rarely blocks
+    if (use_tma && threadIdx.x == 0 && c + 1 < cend) {
+      if (it > 0) mbar_wait(&sDone[(it - 1) & 1], (unsigned)(((it - 1) >> 1) & 1));
+      tma_plane(p + R + 1);
+    }
+#endif
     // ---- pass 2: face-point columns.  The A operand of a chunk of stencil q
     // is the transformed value scaled by the lane's cell's c_q, so ONE
     // accumulator chain per (variable, point) runs through all stencils and
@@ -628,6 +700,9 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     PHASE_MARK(3);
     if constexpr (LB) {  // the next plane's transform quantities, hidden by the epilogue
       __syncwarp();
+#ifndef KFVM_U_CTASYNC
+      if (use_tma && lane == 0) mbar_arrive(&sDone[it & 1]);  // done with the oldest plane
+#endif
       if (c + 1 < cend) load_t(p + 1);
       __pipeline_commit();
     }
@@ -760,6 +835,11 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     }
     PHASE_MARK(4);
     __pipeline_wait_prior(0);
+#ifndef KFVM_U_CTASYNC
+    if (use_tma)
+      __syncwarp();  // load_t's words are the warp's own
+    else
+#endif
     __syncthreads();
     PHASE_MARK(5);
   }
