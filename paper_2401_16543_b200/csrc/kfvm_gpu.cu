@@ -150,6 +150,8 @@ constexpr int npoints(int dim, int R) { return dim == 2 ? 4 * R : 6 * R * R; }
 #include "kfvm_recon.cuh"
 #include "kfvm_recon_u.cuh"
 #include "kfvm_recon_row.cuh"
+constexpr int kWideRows = 4;  // rows of cells per k_states_w CTA
+#include "kfvm_recon_w.cuh"
 #include "kfvm_fused3.cuh"
 
 // ------------------------------------------------------------------ k_flux
@@ -705,6 +707,9 @@ struct kfvm_handle {
   double *St = nullptr, *F = nullptr, *aos = nullptr;
   double* Lb = nullptr;  // 3-D R=2 tensor engine: limiter bounds [3][extended cell] (inside St)
   CUtensorMap* d_tmap = nullptr;  // 3-D R=2: TMA maps of U0, Ua, Ub (ring-plane boxes)
+  CUtensorMap* d_tmapw = nullptr; // ... with the 16-warp engine's box (k_states_w: 2R+4 rows)
+  int* d_gatw = nullptr;          // k_states_w's slot tables
+  int wide = 1;                   // 3-D R=2: the 16-warp W-cache engine where its TMA boxes apply
   int tma = 1;                    // option "tma": ring planes by TMA when the segments allow
   int ring_tiles = 1;             // option "ring_tiles": ring columns on the tensor engine
   size_t st_elems = 0, f_elems = 0, aos_elems = 0;
@@ -1031,6 +1036,18 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
     const CUtensorMap* tm = nullptr;
     if (LB && xsp && h->tma && h->d_tmap)
       tm = U == h->U0 ? h->d_tmap : (U == h->Ua ? h->d_tmap + 1 : (U == h->Ub ? h->d_tmap + 2 : nullptr));
+    bool wide = false;
+    if constexpr (LB) {
+      if (tm && h->wide && h->d_tmapw && h->d_gatw) {  // the 16-warp W-cache engine
+        wide = true;
+        const long long nbw = (long long)((ch.ex - 2 * xsp + 31) / 32) *
+                              ((ch.em + kWideRows - 1) / kWideRows) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
+        k_states_w<kWideRows><<<(unsigned)nbw, 128 * kWideRows, WCfg<kWideRows>::bytes(), h->stream>>>(
+            h->Pr, h->St, h->g, ch, KZ, h->d_Bd, h->d_Bf, h->d_gatw, xsp, h->Lb,
+            h->d_tmapw + (tm - h->d_tmap));
+      }
+    }
+    if (!wide)
     k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(LB), h->stream>>>(
         U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, nullptr, xsp, h->Lb, tm);
     ring();
@@ -1712,6 +1729,17 @@ int make_tmaps(kfvm_handle* h) {
   }
   CK(cudaMalloc(&h->d_tmap, sizeof(maps)));
   CK(cudaMemcpy(h->d_tmap, maps, sizeof(maps), cudaMemcpyHostToDevice));
+  // the 16-warp engine's boxes: 4 rows of cells per CTA (rows past the grid
+  // are zero-filled by the TMA unit and never stored)
+  box[1] = (cuuint32_t)WCfg<kWideRows>::RY;
+  for (int i = 0; i < 3; ++i) {
+    CUresult r = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, bufs[i], dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(h, KFVM_ERR_DEVICE, "cuTensorMapEncodeTiled failed");
+  }
+  CK(cudaMalloc(&h->d_tmapw, sizeof(maps)));
+  CK(cudaMemcpy(h->d_tmapw, maps, sizeof(maps), cudaMemcpyHostToDevice));
   return KFVM_OK;
 }
 
@@ -1854,6 +1882,46 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
     }
     CK(cudaMalloc(&h->d_gat4c, gc.size() * sizeof(int)));
     CK(cudaMemcpy(h->d_gat4c, gc.data(), gc.size() * sizeof(int), cudaMemcpyHostToDevice));
+    // k_states_w's slot words: region offset | (oz + R) << 9 | stencil << 12 |
+    // S0 cell << 16 | last chunk of the stencil << 22; the pass-1 chunks
+    // (front-padded per stencil), then the packed pass-2 chunks
+    using WC = WCfg<kWideRows>;
+    std::vector<int> gw((size_t)WC::NT1 + WC::NT2, 0);
+    for (int q = 0, ck = 0; q < G::NS; ++q) {
+      const int N = t->size[q], o = t->cell_offset[q];
+      const int kcq = (N + 3) / 4, pad = 4 * kcq - N;
+      for (int jj = 0; jj < kcq; ++jj, ++ck)
+        for (int k = 0; k < 4; ++k) {
+          const int hh = 4 * jj + k - pad;
+          const int e = t->gather[o + (hh < 0 ? 0 : hh)];
+          const int inpl = (G::OFF[e][1] + R) * M::RX + G::OFF[e][0] + R;
+          gw[(size_t)ck * 4 + k] = inpl | ((G::OFF[e][2] + R) << 9) | (q << 12) | (e << 16) |
+                                   (jj == kcq - 1 ? 1 << 22 : 0);
+        }
+    }
+    {
+      int sl = 0;
+      for (int q = 0; q < G::NS; ++q) {
+        const int N = t->size[q], o = t->cell_offset[q];
+        for (int hh = 0; hh < N; ++hh, ++sl) {
+          const int e = t->gather[o + hh];
+          const int inpl = (G::OFF[e][1] + R) * M::RX + G::OFF[e][0] + R;
+          gw[(size_t)WC::NT1 + sl] = inpl | ((G::OFF[e][2] + R) << 9) | (q << 12) | (e << 16);
+        }
+      }
+      for (; sl < WC::NT2; ++sl) gw[(size_t)WC::NT1 + sl] = gw[(size_t)WC::NT1 + sl - 1];
+    }
+    // stencil 0 must list every cell of S0 (the W cache is filled from it)
+    {
+      std::vector<char> seen(G::N0, 0);
+      for (int hh = 0; hh < t->size[0]; ++hh) seen[t->gather[t->cell_offset[0] + hh]] = 1;
+      for (int e = 0; e < G::N0; ++e)
+        if (!seen[e]) return fail(h, KFVM_ERR_CONFIG, "stencil 0 does not cover S0");
+    }
+    CK(cudaMalloc(&h->d_gatw, gw.size() * sizeof(int)));
+    CK(cudaMemcpy(h->d_gatw, gw.data(), gw.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaFuncSetAttribute(k_states_w<kWideRows>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)WC::bytes()));
   }
   CK(cudaMalloc(&h->d_Bd, bd.size() * sizeof(double)));
   CK(cudaMalloc(&h->d_Bf, bf.size() * sizeof(double)));
@@ -2249,7 +2317,7 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
       im = DeviceImage();
     }
   }
-  for (void* p : {(void*)h->d_gat4c, (void*)h->d_tmap, (void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
+  for (void* p : {(void*)h->d_gat4c, (void*)h->d_gatw, (void*)h->d_tmapw, (void*)h->d_tmap, (void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
                   (void*)h->aos, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
                   (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_gat8, (void*)h->d_edges, (void*)h->d_tt,
@@ -2699,6 +2767,11 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
   if (n == "tma") {
     drop_graphs(h);
     h->tma = value ? 1 : 0;
+    return KFVM_OK;
+  }
+  if (n == "wide") {  // 3-D R=2: 1 = the 16-warp W-cache engine (k_states_w), 0 = k_states_u
+    drop_graphs(h);
+    h->wide = value ? 1 : 0;
     return KFVM_OK;
   }
   if (n == "ring_split") {

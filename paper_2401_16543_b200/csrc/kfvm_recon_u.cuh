@@ -12,7 +12,7 @@
 //
 // Work decomposition.  CTA = 4 warps = a 32-cell x-segment of one row; it
 // marches along the slab axis over KZ extended planes.  Warp w owns cells
-// w, w+4, .., w+28 of the segment and ALL variables: the DMMA A operand (8 cells x 4
+// seg_cell(w, 0..7) of the segment and ALL variables: the DMMA A operand (8 cells x 4
 // stencil entries) is transformed on the fly from the staged U region, B (4
 // entries x 8 columns) is the weight table in fragment order.  The accumulator layout
 // puts all nv variables of one (cell, column) in one thread, so Phi, the
@@ -27,6 +27,18 @@
 #define KFVM_U_UNR 4
 #endif
 constexpr int kUChunkUnroll = KFVM_U_UNR;
+// Cell of the 32-cell segment owned by quad r8 of warp w: 8 contiguous cells
+// per warp.  A chunk's four slots sit at arbitrary (x, row, plane) offsets of
+// the region, and row and plane strides are multiples of 4 words, so with the
+// cells of a warp 4 apart (w + 4 r8) two slots with equal x offsets mod 4 put
+// 16 distinct words on 8 banks: measured 4.0-4.6 wavefronts per A-operand
+// load against 2.1-2.4 with contiguous cells (bank model of the chunk tables
+// = the ncu count), and the stores of a warp's 8 cells fill two sectors.
+#ifdef KFVM_CELL_STRIDE4
+__device__ __forceinline__ int seg_cell(int w, int r8) { return w + 4 * r8; }
+#else
+__device__ __forceinline__ int seg_cell(int w, int r8) { return 8 * w + r8; }
+#endif
 #ifndef KFVM_U_MINB
 #define KFVM_U_MINB 2
 #endif
@@ -164,7 +176,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   // [var][36 rows][5 columns] (the same size), the host passes the chunk
   // tables built for that layout, and the planes load by cp.async.
   int bid = blockIdx.x;
-  int seg = 0, zblk, b, j0, a, cidx = w + 4 * r8;
+  int seg = 0, zblk, b, j0, a, cidx = seg_cell(w, r8);
   if (LB && col) {
     const int nys = (ch.em + 31) >> 5;
     const int side = bid & 1;
@@ -187,9 +199,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   const int j = (LB && col) ? b - 1 : j0;  // this lane's cell's mid index
   // region origin: x of column 0 (+R) and mid index of row 0 (+R)
   const int x0 = (LB && col) ? a - 1 : xsp + seg * 32 - 1;
-  // warp w owns the cells w, w+4, ..., w+28 of the segment (stride 4): the 4
-  // slots of a DMMA chunk are mostly consecutive x offsets, and with stride-4
-  // rows the 16 (cell, slot) words of a half-warp fall in distinct banks
+  // warp w owns the cells seg_cell(w, 0..7) of the segment
   const bool active = (LB && col) ? b < ch.em : a < ch.ex - xsp;
   const int sx = 0;
   const bool use_tma = LB && tmap != nullptr && !col;
@@ -279,7 +289,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   // cells for plane q, staged in the warp's weight area sCw[f][cell] (free
   // from the end of pass 2 until the next plane's transform is read)
   auto load_t = [&](int q) {
-    const int f = lane >> 3, cc = w + 4 * (lane & 7);
+    const int f = lane >> 3, cc = seg_cell(w, lane & 7);
     const int ac = (LB && col) ? a : min(xsp + seg * 32 + cc, ch.ex - 1);
     const int jc = (LB && col) ? min(seg * 32 + cc, ch.em - 1) - 1 : j;
     __pipeline_memcpy_async(sCw + f * 8 + (lane & 7),
