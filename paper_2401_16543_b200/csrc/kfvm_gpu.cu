@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1731,6 +1732,7 @@ int make_tmaps(kfvm_handle* h) {
   CK(cudaMemcpy(h->d_tmap, maps, sizeof(maps), cudaMemcpyHostToDevice));
   // the 16-warp engine's boxes: 4 rows of cells per CTA (rows past the grid
   // are zero-filled by the TMA unit and never stored)
+  box[0] = (cuuint32_t)WCfg<kWideRows>::RX;
   box[1] = (cuuint32_t)WCfg<kWideRows>::RY;
   for (int i = 0; i < 3; ++i) {
     CUresult r = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, bufs[i], dims, strides, box, es,
@@ -1883,9 +1885,98 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
     CK(cudaMalloc(&h->d_gat4c, gc.size() * sizeof(int)));
     CK(cudaMemcpy(h->d_gat4c, gc.data(), gc.size() * sizeof(int), cudaMemcpyHostToDevice));
     // k_states_w's slot words: region offset | (oz + R) << 9 | stencil << 12 |
-    // S0 cell << 16 | last chunk of the stencil << 22; the pass-1 chunks
-    // (front-padded per stencil), then the packed pass-2 chunks
+    // W-cache position of the S0 cell << 16 | last chunk of the stencil << 22;
+    // the pass-1 chunks (front-padded per stencil), then the packed pass-2 chunks
     using WC = WCfg<kWideRows>;
+    // stencil 0 must list every cell of S0 (the W cache is filled from it)
+    {
+      std::vector<char> seen(G::N0, 0);
+      for (int hh = 0; hh < t->size[0]; ++hh) seen[t->gather[t->cell_offset[0] + hh]] = 1;
+      for (int e = 0; e < G::N0; ++e)
+        if (!seen[e]) return fail(h, KFVM_ERR_CONFIG, "stencil 0 does not cover S0");
+    }
+    // the chunks that READ the cache: pass 1 from stencil 1 on, all of pass 2
+    std::vector<std::array<int, 4>> rd;
+    for (int q = 1; q < G::NS; ++q) {
+      const int N = t->size[q], o = t->cell_offset[q];
+      const int kcq = (N + 3) / 4, pad = 4 * kcq - N;
+      for (int jj = 0; jj < kcq; ++jj) {
+        std::array<int, 4> c;
+        for (int k = 0; k < 4; ++k) c[k] = t->gather[o + std::max(4 * jj + k - pad, 0)];
+        rd.push_back(c);
+      }
+    }
+    {
+      std::vector<int> flat;
+      for (int q = 0; q < G::NS; ++q)
+        for (int hh = 0; hh < t->size[q]; ++hh) flat.push_back(t->gather[t->cell_offset[q] + hh]);
+      while (flat.size() % 4) flat.push_back(flat.back());
+      for (size_t i = 0; i < flat.size(); i += 4) rd.push_back({flat[i], flat[i + 1], flat[i + 2], flat[i + 3]});
+    }
+    // 4-colouring of S0 (bank window of a cell's cache row = colour): minimise
+    // the half-warp wavefronts, sum over chunks of the largest number of
+    // distinct cells of one colour; balanced colours (N0 positions suffice);
+    // seeded multi-start pair-swap descent, deterministic
+    std::vector<int> col(G::N0), bestc;
+    auto cost = [&](const std::vector<int>& c) {
+      int tot = 0;
+      for (const auto& ck : rd) {
+        int cnt[4] = {0, 0, 0, 0};
+        for (int k = 0; k < 4; ++k) {
+          bool dup = false;
+          for (int k2 = 0; k2 < k; ++k2) dup |= ck[k2] == ck[k];
+          if (!dup) cnt[c[ck[k]]]++;
+        }
+        tot += std::max(std::max(cnt[0], cnt[1]), std::max(cnt[2], cnt[3]));
+      }
+      return tot;
+    };
+    int bestv = 1 << 30;
+    unsigned long long rng = 0x9e3779b97f4a7c15ull;
+    for (int trial = 0; trial < 64; ++trial) {
+      std::vector<int> perm(G::N0);
+      for (int e = 0; e < G::N0; ++e) perm[e] = e;
+      for (int e = G::N0 - 1; e > 0; --e) {
+        rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+        std::swap(perm[e], perm[(int)((rng >> 33) % (unsigned)(e + 1))]);
+      }
+      for (int i = 0; i < G::N0; ++i) col[perm[i]] = i % 4;
+      int cv = cost(col);
+      for (bool imp = true; imp;) {
+        imp = false;
+        for (int a2 = 0; a2 < G::N0; ++a2)
+          for (int b2 = a2 + 1; b2 < G::N0; ++b2) {
+            if (col[a2] == col[b2]) continue;
+            std::swap(col[a2], col[b2]);
+            const int c2 = cost(col);
+            if (c2 < cv) {
+              cv = c2;
+              imp = true;
+            } else {
+              std::swap(col[a2], col[b2]);
+            }
+          }
+      }
+      if (cv < bestv) {
+        bestv = cv;
+        bestc = col;
+      }
+    }
+    // position of a cell: the next free one with position mod 4 = colour
+    // (i % 4 colours: sizes 9, 8, 8, 8 -> the 9 of colour 0 end at position 32)
+    std::vector<int> pos(G::N0);
+    {
+      int cnt[4] = {0, 0, 0, 0}, big = 0;
+      for (int e = 0; e < G::N0; ++e) cnt[bestc[e]]++;
+      for (int k = 1; k < 4; ++k)
+        if (cnt[k] > cnt[big]) big = k;
+      int nxt[4] = {0, 0, 0, 0};
+      for (int e = 0; e < G::N0; ++e) {
+        const int c = bestc[e] == big ? 0 : (bestc[e] == 0 ? big : bestc[e]);  // largest colour first
+        pos[e] = c + 4 * nxt[c]++;
+        if (pos[e] >= G::N0) return fail(h, KFVM_ERR_CONFIG, "W-cache colouring does not fit");
+      }
+    }
     std::vector<int> gw((size_t)WC::NT1 + WC::NT2, 0);
     for (int q = 0, ck = 0; q < G::NS; ++q) {
       const int N = t->size[q], o = t->cell_offset[q];
@@ -1894,8 +1985,8 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
         for (int k = 0; k < 4; ++k) {
           const int hh = 4 * jj + k - pad;
           const int e = t->gather[o + (hh < 0 ? 0 : hh)];
-          const int inpl = (G::OFF[e][1] + R) * M::RX + G::OFF[e][0] + R;
-          gw[(size_t)ck * 4 + k] = inpl | ((G::OFF[e][2] + R) << 9) | (q << 12) | (e << 16) |
+          const int inpl = (G::OFF[e][1] + R) * WC::RX + G::OFF[e][0] + R;
+          gw[(size_t)ck * 4 + k] = inpl | ((G::OFF[e][2] + R) << 9) | (q << 12) | (pos[e] << 16) |
                                    (jj == kcq - 1 ? 1 << 22 : 0);
         }
     }
@@ -1905,18 +1996,11 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
         const int N = t->size[q], o = t->cell_offset[q];
         for (int hh = 0; hh < N; ++hh, ++sl) {
           const int e = t->gather[o + hh];
-          const int inpl = (G::OFF[e][1] + R) * M::RX + G::OFF[e][0] + R;
-          gw[(size_t)WC::NT1 + sl] = inpl | ((G::OFF[e][2] + R) << 9) | (q << 12) | (e << 16);
+          const int inpl = (G::OFF[e][1] + R) * WC::RX + G::OFF[e][0] + R;
+          gw[(size_t)WC::NT1 + sl] = inpl | ((G::OFF[e][2] + R) << 9) | (q << 12) | (pos[e] << 16);
         }
       }
       for (; sl < WC::NT2; ++sl) gw[(size_t)WC::NT1 + sl] = gw[(size_t)WC::NT1 + sl - 1];
-    }
-    // stencil 0 must list every cell of S0 (the W cache is filled from it)
-    {
-      std::vector<char> seen(G::N0, 0);
-      for (int hh = 0; hh < t->size[0]; ++hh) seen[t->gather[t->cell_offset[0] + hh]] = 1;
-      for (int e = 0; e < G::N0; ++e)
-        if (!seen[e]) return fail(h, KFVM_ERR_CONFIG, "stencil 0 does not cover S0");
     }
     CK(cudaMalloc(&h->d_gatw, gw.size() * sizeof(int)));
     CK(cudaMemcpy(h->d_gatw, gw.data(), gw.size() * sizeof(int), cudaMemcpyHostToDevice));

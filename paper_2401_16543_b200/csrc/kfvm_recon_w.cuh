@@ -28,7 +28,12 @@ struct WCfg {
   using C = UCfg<3, 2>;
   static constexpr int R = 2, nv = 5;
   static constexpr int NW = 4 * MR;                  // warps
-  static constexpr int RX = 32 + 2 * R;              // region x extent
+  // region x extent: 36 columns are needed; rows 42 words apart (and the
+  // warp's 8 cells contiguous) spread the four slots of a chunk — arbitrary
+  // (x, row) offsets of the stencil — over the banks: 2.1 wavefronts per
+  // A-operand load in the half-warp bank model of the chunk tables against
+  // 3.4 at 36 (ncu: the model's numbers); the 6 extra columns ride in the box
+  static constexpr int RX = 42;
   static constexpr int RY = 2 * R + MR;              // region rows
   static constexpr int RROW = RY * RX;               // one variable of a plane
   static constexpr int PL = nv * RROW;               // one region plane
@@ -37,7 +42,14 @@ struct WCfg {
   static constexpr int SCW = G::NS * nv * 8;         // beta / c_q per warp
   static constexpr int V0 = 2, NCV = nv - V0;        // cached variables V0 .. nv-1
   static constexpr int N0 = G::N0;                   // cells of S0
-  static constexpr int WCW = NCV * N0 * 8;           // W cache per warp [v][cell of S0][8 cells]
+  // W cache per warp [v][half h of the 8 cells][position 0..N0-1][4 cells]: a
+  // 64-bit load runs per half-warp (4 cells x 4 slots), which is conflict-free
+  // when the four S0 cells sit in different 4-word bank windows — position mod
+  // 4, a 4-colouring of S0 the host searches so that the cells of (nearly)
+  // every chunk differ (upload_gen: 1.2 wavefronts per half against 2.1 with
+  // rows of 8 cells)
+  static constexpr int HP = N0 * 4;
+  static constexpr int WCW = NCV * 2 * HP;
   static constexpr int K0 = G::kc(0);                // chunks of stencil 0
   static constexpr int NT1 = 4 * G::NCHUNK, NT2 = 4 * C::NCH2;  // table words
   static constexpr size_t bytes() {
@@ -47,7 +59,8 @@ struct WCfg {
 };
 
 // table word of a chunk slot (host: upload_gen): region offset (oy+R)*RX+ox+R
-// | (oz+R) << 9 | stencil << 12 | S0 cell << 16 | last chunk of its stencil << 22
+// | (oz+R) << 9 | stencil << 12 | W-cache position of the S0 cell << 16 | last
+// chunk of its stencil << 22
 template <int MR>
 __global__ void __launch_bounds__(128 * MR, 1)
     k_states_w(const double* __restrict__ Pr, double* __restrict__ St, Geo g, Chunk ch, int KZ,
@@ -118,7 +131,7 @@ __global__ void __launch_bounds__(128 * MR, 1)
   __syncthreads();
 
   double* sCw = sC + w * W::SCW;
-  double* sWw = sWc + w * W::WCW + r8;  // + (v - V0) * N0 * 8 + e * 8
+  double* sWw = sWc + w * W::WCW + (r8 >> 2) * W::HP + (r8 & 3);  // + (v - V0) * 2 HP + 4 position
   // the transform's per-cell quantities (1/rho, u_d) of the warp's 8 cells for
   // plane q, staged in the warp's weight area (see k_states_u)
   auto load_t = [&](int q) {
@@ -141,7 +154,7 @@ __global__ void __launch_bounds__(128 * MR, 1)
   // TMAs (at the top of its plane, when every other warp has long arrived),
   // which also keeps any warp from running a full plane ahead of it.
 #ifndef KFVM_W_SKEW_NS
-#define KFVM_W_SKEW_NS 9000
+#define KFVM_W_SKEW_NS 3000
 #endif
   if (wr > 0) __nanosleep(wr * KFVM_W_SKEW_NS);
   const bool issuer = threadIdx.x == 128 * (MR - 1);
@@ -230,9 +243,9 @@ __global__ void __launch_bounds__(128 * MR, 1)
           double aw[nv];
 #pragma unroll
           for (int v = 0; v < nv; ++v) aw[v] = phi_row<D>(T, av, v);
-          double* wc = sWw + ((wd >> 16) & 63) * 8;
+          double* wc = sWw + ((wd >> 16) & 63) * 4;
 #pragma unroll
-          for (int v = V0; v < nv; ++v) wc[(v - V0) * W::N0 * 8] = aw[v];
+          for (int v = V0; v < nv; ++v) wc[(v - V0) * 2 * W::HP] = aw[v];
 #pragma unroll
           for (int v = 0; v < nv; ++v) dmma(acc[v][0], acc[v][1], aw[v], bv);
 #pragma unroll
@@ -254,9 +267,9 @@ __global__ void __launch_bounds__(128 * MR, 1)
           const double* ap = plane((wd >> 9) & 7) + (wd & 511) + cb;
           a0 = ap[0];
           a1 = ap[RROW];
-          const double* wc = sWw + ((wd >> 16) & 63) * 8;
+          const double* wc = sWw + ((wd >> 16) & 63) * 4;
 #pragma unroll
-          for (int v = 0; v < NCV; ++v) aw2[v] = wc[v * W::N0 * 8];
+          for (int v = 0; v < NCV; ++v) aw2[v] = wc[v * 2 * W::HP];
           bv = Bd[(W::K0 * ND) * 32 + lane];
           bt = Bd[(W::K0 * ND + ND - 1) * 32 + k4];
         }
@@ -266,10 +279,10 @@ __global__ void __launch_bounds__(128 * MR, 1)
           const int wn = sT1[cn * 4 + k4];
           const double* ap = plane((wn >> 9) & 7) + (wn & 511) + cb;
           const double n0 = ap[0], n1 = ap[RROW];
-          const double* wc = sWw + ((wn >> 16) & 63) * 8;
+          const double* wc = sWw + ((wn >> 16) & 63) * 4;
           double an2[NCV];
 #pragma unroll
-          for (int v = 0; v < NCV; ++v) an2[v] = wc[v * W::N0 * 8];
+          for (int v = 0; v < NCV; ++v) an2[v] = wc[v * 2 * W::HP];
           const double bn = Bd[(cn * ND) * 32 + lane];
           const double btn = Bd[(cn * ND + ND - 1) * 32 + k4];
           double aw[nv];
@@ -361,9 +374,9 @@ __global__ void __launch_bounds__(128 * MR, 1)
         const double* ap = plane((wd >> 9) & 7) + (wd & 511) + cb;
         a0 = ap[0];
         a1 = ap[RROW];
-        const double* wc = sWw + ((wd >> 16) & 63) * 8;
+        const double* wc = sWw + ((wd >> 16) & 63) * 4;
 #pragma unroll
-        for (int v = 0; v < NCV; ++v) aw2[v] = wc[v * W::N0 * 8];
+        for (int v = 0; v < NCV; ++v) aw2[v] = wc[v * 2 * W::HP];
 #pragma unroll
         for (int n = 0; n < NPT; ++n) bv[n] = ldB2(Bf2 + n * 32 + lane);
       }
@@ -373,10 +386,10 @@ __global__ void __launch_bounds__(128 * MR, 1)
         const int wn = sT2[cn * 4 + k4];
         const double* ap = plane((wn >> 9) & 7) + (wn & 511) + cb;
         const double n0 = ap[0], n1 = ap[RROW];
-        const double* wc = sWw + ((wn >> 16) & 63) * 8;
+        const double* wc = sWw + ((wn >> 16) & 63) * 4;
         double an2[NCV], bn[NPT];
 #pragma unroll
-        for (int v = 0; v < NCV; ++v) an2[v] = wc[v * W::N0 * 8];
+        for (int v = 0; v < NCV; ++v) an2[v] = wc[v * 2 * W::HP];
 #pragma unroll
         for (int n = 0; n < NPT; ++n) bn[n] = ldB2(Bf2 + (cn * NPT + n) * 32 + lane);
         const int qa = (wd >> 12) & 7;

@@ -10,5 +10,5 @@ timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; ec
 timeout 600 python bench.py --config 2 > gpurun_out/bench_c2.log 2>&1; echo "rc=$?" >> gpurun_out/bench_c2.log
 timeout 600 python bench.py --config 3 > gpurun_out/bench_c3.log 2>&1; echo "rc=$?" >> gpurun_out/bench_c3.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv python tools/profile_step.py --config 4 --steps 1 > gpurun_out/ncu_l.log 2>&1
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_states_u -s 2 -c 1 -o gpurun_out/prof_c4_states python tools/profile_step.py --config 4 --steps 1 > gpurun_out/ncu_full.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_states_w -s 2 -c 1 -o gpurun_out/prof_c4_states_w python tools/profile_step.py --config 4 --steps 1 > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
