@@ -825,6 +825,14 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
         }
     thp = fmin(thp, __shfl_xor_sync(0xffffffffu, thp, 1));
     thp = fmin(thp, __shfl_xor_sync(0xffffffffu, thp, 2));
+    if (thp < 1.0) {  // (a branch: the scaling is rare, its FP64 operations are not)
+#pragma unroll
+      for (int n = 0; n < NPT; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int v = 0; v < nv; ++v) st[n][e][v] = fma(thp, st[n][e][v] - Ubar[v], Ubar[v]);
+    }
     if (active) {
       const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
 #pragma unroll
@@ -834,10 +842,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
           const int sp = 8 * n + 2 * k4 + e;
           if (sp < NP) {
 #pragma unroll
-            for (int v = 0; v < nv; ++v) {
-              const double u = thp < 1.0 ? fma(thp, st[n][e][v] - Ubar[v], Ubar[v]) : st[n][e][v];
-              St[(long long)(sp * nv + v) * ch.next + tid] = u;
-            }
+            for (int v = 0; v < nv; ++v) St[(long long)(sp * nv + v) * ch.next + tid] = st[n][e][v];
           }
         }
     }
