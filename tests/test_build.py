@@ -48,6 +48,14 @@ def test_3d_tensor_engine_fits_four_ctas_per_sm():
         assert regs <= 128 and st <= 64 and ld <= 64, (k, regs, st, ld)
 
 
+def test_3d_wide_engine_fits_one_cta_per_sm():
+    """k_states_w<4>: 512 threads at 128 registers (the whole register file of
+    an SM) with a small documented spill (kfvm_recon_w.cuh)."""
+    ks = kernels()
+    for k, (regs, st, ld) in pick(ks, re.escape("k_states_w<4>")).items():
+        assert regs <= 128 and st <= 64 and ld <= 64, (k, regs, st, ld)
+
+
 def test_2d_flux_spill_budget_as_documented():
     """2-D k_flux runs at 64 registers (8 CTAs/SM) and spills a documented
     amount (kfvm_gpu.cu comment above k_flux)."""
