@@ -709,8 +709,7 @@ struct kfvm_handle {
   double* Lb = nullptr;  // 3-D R=2 tensor engine: limiter bounds [3][extended cell] (inside St)
   CUtensorMap* d_tmap = nullptr;  // 3-D R=2: TMA maps of U0, Ua, Ub (ring-plane boxes)
   CUtensorMap* d_tmapw = nullptr; // ... with the 16-warp engine's box (k_states_w: 2R+4 rows)
-  int* d_gatw = nullptr;          // k_states_w's pass-2 slot words
-  void* d_slot1 = nullptr;        // k_states_w's pass-1 slots (WSlot)
+  int* d_gatw = nullptr;          // k_states_w's slot tables
   int wide = 1;                   // 3-D R=2: the 16-warp W-cache engine where its TMA boxes apply
   int tma = 1;                    // option "tma": ring planes by TMA when the segments allow
   int ring_tiles = 1;             // option "ring_tiles": ring columns on the tensor engine
@@ -1045,8 +1044,7 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
         const long long nbw = (long long)((ch.ex - 2 * xsp + 31) / 32) *
                               ((ch.em + kWideRows - 1) / kWideRows) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
         k_states_w<kWideRows><<<(unsigned)nbw, 128 * kWideRows, WCfg<kWideRows>::bytes(), h->stream>>>(
-            h->Pr, h->St, h->g, ch, KZ, h->d_Bd, h->d_Bf, (const WSlot*)h->d_slot1, h->d_gatw, xsp,
-            h->Lb,
+            h->Pr, h->St, h->g, ch, KZ, h->d_Bd, h->d_Bf, h->d_gatw, xsp, h->Lb,
             h->d_tmapw + (tm - h->d_tmap));
       }
     }
@@ -2004,13 +2002,8 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
       }
       for (; sl < WC::NT2; ++sl) gw[(size_t)WC::NT1 + sl] = gw[(size_t)WC::NT1 + sl - 1];
     }
-    std::vector<WSlot> s1(WC::NT1);
-    for (int i = 0; i < WC::NT1; ++i)  // tail weight of slot k of chunk ck: lane k of the last tile
-      s1[i] = WSlot{gw[i], 0, bd[((size_t)(i / 4) * M::ND + M::ND - 1) * 32 + i % 4]};
-    CK(cudaMalloc(&h->d_slot1, s1.size() * sizeof(WSlot)));
-    CK(cudaMemcpy(h->d_slot1, s1.data(), s1.size() * sizeof(WSlot), cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&h->d_gatw, WC::NT2 * sizeof(int)));
-    CK(cudaMemcpy(h->d_gatw, gw.data() + WC::NT1, WC::NT2 * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&h->d_gatw, gw.size() * sizeof(int)));
+    CK(cudaMemcpy(h->d_gatw, gw.data(), gw.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaFuncSetAttribute(k_states_w<kWideRows>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)WC::bytes()));
   }
@@ -2408,7 +2401,7 @@ extern "C" void kfvm_gpu_destroy(kfvm_handle* h) {
       im = DeviceImage();
     }
   }
-  for (void* p : {(void*)h->d_gat4c, (void*)h->d_gatw, h->d_slot1, (void*)h->d_tmapw, (void*)h->d_tmap, (void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
+  for (void* p : {(void*)h->d_gat4c, (void*)h->d_gatw, (void*)h->d_tmapw, (void*)h->d_tmap, (void*)h->U0, (void*)h->Ua, (void*)h->Ub, (void*)h->Pr, (void*)h->St, (void*)h->F,
                   (void*)h->aos, (void*)h->d_dt_seq,
                   (void*)h->d_dt_cur, (void*)h->d_smax, (void*)h->d_step, (void*)h->d_err,
                   (void*)h->d_Bd, (void*)h->d_Bf, (void*)h->d_gat4, (void*)h->d_gat8, (void*)h->d_edges, (void*)h->d_tt,

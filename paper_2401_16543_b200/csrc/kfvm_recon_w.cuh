@@ -53,17 +53,9 @@ struct WCfg {
   static constexpr int K0 = G::kc(0);                // chunks of stencil 0
   static constexpr int NT1 = 4 * G::NCHUNK, NT2 = 4 * C::NCH2;  // table words
   static constexpr size_t bytes() {
-    return sizeof(double) * (RING * SL + NW * SCW + NW * WCW + 2 * NT1) +
-           sizeof(int) * ((NT2 + 1) & ~1) + sizeof(unsigned long long) * (RING + 2);
+    return sizeof(double) * (RING * SL + NW * SCW + NW * WCW) +
+           sizeof(int) * ((NT1 + NT2 + 1) & ~1) + sizeof(unsigned long long) * (RING + 2);
   }
-};
-
-// pass-1 chunk slot: the table word and the slot's tail-derivative weight
-// (column 8 of the derivative table: one 128-bit shared load per chunk
-// instead of a table word and a global load)
-struct __align__(16) WSlot {
-  int w, pad;
-  double bt;
 };
 
 // table word of a chunk slot (host: upload_gen): region offset (oy+R)*RX+ox+R
@@ -73,8 +65,7 @@ template <int MR>
 __global__ void __launch_bounds__(128 * MR, 1)
     k_states_w(const double* __restrict__ Pr, double* __restrict__ St, Geo g, Chunk ch, int KZ,
                const double* __restrict__ Bd, const double* __restrict__ Bf,
-               const WSlot* __restrict__ slot1, const int* __restrict__ gatw, int xsp,
-               const double* __restrict__ Lb,
+               const int* __restrict__ gatw, int xsp, const double* __restrict__ Lb,
                const CUtensorMap* __restrict__ tmap) {
   using G = Gen<3, 2>;
   using C = UCfg<3, 2>;
@@ -86,16 +77,16 @@ __global__ void __launch_bounds__(128 * MR, 1)
   double* sRing = smem;                                // [RING][nv][RY][RX]
   double* sC = sRing + W::RING * SL;                   // [warp][q][v][8]
   double* sWc = sC + W::NW * W::SCW;                   // [warp][v - V0][S0 cell][8]
-  WSlot* sT1 = reinterpret_cast<WSlot*>(sWc + W::NW * W::WCW);  // pass-1 slots [chunk][4]
-  int* sT2 = reinterpret_cast<int*>(sT1 + W::NT1);     // pass-2 slots (packed chunks) [chunk][4]
-  unsigned long long* sBar = reinterpret_cast<unsigned long long*>(sT2 + ((W::NT2 + 1) & ~1));
+  int* sT1 = reinterpret_cast<int*>(sWc + W::NW * W::WCW);  // pass-1 slots [chunk][4]
+  int* sT2 = sT1 + W::NT1;                             // pass-2 slots (packed chunks) [chunk][4]
+  unsigned long long* sBar =
+      reinterpret_cast<unsigned long long*>(sT1 + ((W::NT1 + W::NT2 + 1) & ~1));
   unsigned long long* sDone = sBar + W::RING;
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int k4 = lane & 3, r8 = lane >> 2;
   const int wr = w >> 2, wx = w & 3;  // the warp's row of the CTA, its cell phase
-  for (int i = threadIdx.x; i < W::NT1; i += 128 * MR) sT1[i] = slot1[i];
-  for (int i = threadIdx.x; i < W::NT2; i += 128 * MR) sT2[i] = gatw[i];
+  for (int i = threadIdx.x; i < W::NT1 + W::NT2; i += 128 * MR) sT1[i] = gatw[i];
 
   int bid = blockIdx.x;
   const int nseg = (ch.ex - 2 * xsp + 31) >> 5;
@@ -231,27 +222,24 @@ __global__ void __launch_bounds__(128 * MR, 1)
       // -- stencil 0 (= S0): raw values, transformed here and cached
       {
         double av[nv], bv, bt;
-        int wd;
+        int wd = sT1[k4];
         {
-          const WSlot s0 = sT1[k4];
-          wd = s0.w;
-          bt = s0.bt;
           const double* ap = plane((wd >> 9) & 7) + (wd & 511) + cb;
 #pragma unroll
           for (int u = 0; u < nv; ++u) av[u] = ap[u * RROW];
           bv = Bd[lane];
+          bt = Bd[(ND - 1) * 32 + k4];
         }
 #pragma unroll
         for (int ck = 0; ck < W::K0; ++ck) {
           const int cn = ck + 1 < W::K0 ? ck + 1 : ck;
-          const WSlot sn = sT1[cn * 4 + k4];
-          const int wn = sn.w;
-          const double btn = sn.bt;
+          const int wn = sT1[cn * 4 + k4];
           const double* ap = plane((wn >> 9) & 7) + (wn & 511) + cb;
           double an[nv];
 #pragma unroll
           for (int u = 0; u < nv; ++u) an[u] = ap[u * RROW];
           const double bn = Bd[(cn * ND) * 32 + lane];
+          const double btn = Bd[(cn * ND + ND - 1) * 32 + k4];
           double aw[nv];
 #pragma unroll
           for (int v = 0; v < nv; ++v) aw[v] = phi_row<D>(T, av, v);
@@ -274,11 +262,8 @@ __global__ void __launch_bounds__(128 * MR, 1)
       // -- stencils 1..: rho and m_x raw, the cached W_2.. of the slot's S0 cell
       {
         double a0, a1, aw2[NCV], bv, bt;
-        int wd;
+        int wd = sT1[W::K0 * 4 + k4];
         {
-          const WSlot s0 = sT1[W::K0 * 4 + k4];
-          wd = s0.w;
-          bt = s0.bt;
           const double* ap = plane((wd >> 9) & 7) + (wd & 511) + cb;
           a0 = ap[0];
           a1 = ap[RROW];
@@ -286,13 +271,12 @@ __global__ void __launch_bounds__(128 * MR, 1)
 #pragma unroll
           for (int v = 0; v < NCV; ++v) aw2[v] = wc[v * 2 * W::HP];
           bv = Bd[(W::K0 * ND) * 32 + lane];
+          bt = Bd[(W::K0 * ND + ND - 1) * 32 + k4];
         }
 #pragma unroll kUChunkUnroll
         for (int ck = W::K0; ck < G::NCHUNK; ++ck) {
           const int cn = ck + 1 < G::NCHUNK ? ck + 1 : ck;
-          const WSlot sn = sT1[cn * 4 + k4];
-          const int wn = sn.w;
-          const double btn = sn.bt;
+          const int wn = sT1[cn * 4 + k4];
           const double* ap = plane((wn >> 9) & 7) + (wn & 511) + cb;
           const double n0 = ap[0], n1 = ap[RROW];
           const double* wc = sWw + ((wn >> 16) & 63) * 4;
@@ -300,6 +284,7 @@ __global__ void __launch_bounds__(128 * MR, 1)
 #pragma unroll
           for (int v = 0; v < NCV; ++v) an2[v] = wc[v * 2 * W::HP];
           const double bn = Bd[(cn * ND) * 32 + lane];
+          const double btn = Bd[(cn * ND + ND - 1) * 32 + k4];
           double aw[nv];
           aw[0] = a0;
           aw[1] = fma(-T.ut[0], a0, a1) * T.inv_r;
