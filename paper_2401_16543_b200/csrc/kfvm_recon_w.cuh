@@ -189,6 +189,16 @@ __global__ void __launch_bounds__(128 * MR, 1)
 #pragma unroll
       for (int u = 0; u < nv; ++u) acc[u][0] = acc[u][1] = tl[u] = 0.0;
       int q = 0;
+      // (-DKFVM_W_BETA_PAIRS, bitwise, not the default)
+      // beta of a stencil = ((p0 + sc8 d^2) + p1) + (p2 + p3), with lane k4's
+      // partial chain p_k4 over its two derivative columns and the tail
+      // derivative d = (s0 + s1) + (s2 + s3) of the quad's slot chains (oracle
+      // weno_field order).  The quad reduces TWO stencils at a time: the even
+      // lanes take the earlier one, the odd lanes the later one — in the xor-1
+      // exchanges every lane sends the partner's stencil's value and keeps its
+      // own, so each butterfly step is one add per variable for both stencils
+      // (the same sums: + commutes) instead of one per stencil.
+#ifndef KFVM_W_BETA_PAIRS  // default: one stencil at a time (the pair reduction below measured 828.7 vs 822.4 ms/step on config 4: fewer FP64 operations and shuffles, more selects and registers)
       auto beta = [&]() {
         double bq[nv];
 #pragma unroll
@@ -219,6 +229,50 @@ __global__ void __launch_bounds__(128 * MR, 1)
         for (int u = 0; u < nv; ++u) acc[u][0] = acc[u][1] = 0.0;
         ++q;
       };
+#else
+      static_assert(NS % 2 == 0, "stencils reduce in pairs");
+      double pE[nv], tE[nv];  // the even stencil's partials and tail slot sums
+      auto beta = [&]() {
+        double bq[nv];
+#pragma unroll
+        for (int v = 0; v < nv; ++v) bq[v] = 0.0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double sc = c_t.scale[2 * k4 + e];
+#pragma unroll
+          for (int v = 0; v < nv; ++v) bq[v] = fma(sc, acc[v][e] * acc[v][e], bq[v]);
+        }
+        if (!(q & 1)) {
+#pragma unroll
+          for (int v = 0; v < nv; ++v) {
+            pE[v] = bq[v];
+            tE[v] = tl[v];
+          }
+        } else {
+          const bool odd = k4 & 1;
+          const double sc8 = c_t.scale[8];
+#pragma unroll
+          for (int v = 0; v < nv; ++v) {
+            // tail: own stencil's slot sum + the partner's slot sum of it
+            const double tm = odd ? tl[v] : tE[v], ts = odd ? tE[v] : tl[v];
+            const double u2 = tm + __shfl_xor_sync(0xffffffffu, ts, 1);
+            const double d = u2 + __shfl_xor_sync(0xffffffffu, u2, 2);
+            // partials: lanes 0, 1 end with (p0, p1), lanes 2, 3 with (p2, p3)
+            const double pm = odd ? bq[v] : pE[v], ps = odd ? pE[v] : bq[v];
+            const double pr = __shfl_xor_sync(0xffffffffu, ps, 1);
+            double pa = odd ? pr : pm;
+            const double pb = odd ? pm : pr;
+            if (k4 < 2) pa = fma(sc8, d * d, pa);
+            const double s2 = pa + pb;
+            const double bt2 = s2 + __shfl_xor_sync(0xffffffffu, s2, 2);
+            if (k4 < 2) sCw[((q - 1 + (int)odd) * nv + v) * 8 + r8] = bt2;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < nv; ++u) acc[u][0] = acc[u][1] = tl[u] = 0.0;
+        ++q;
+      };
+#endif
       // -- stencil 0 (= S0): raw values, transformed here and cached
       {
         double av[nv], bv, bt;
