@@ -1049,7 +1049,7 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
       }
     }
     if (!wide)
-    k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(LB), h->stream>>>(
+    k_states_u<DIM, R><<<(unsigned)nblk2, 128, UCfg<DIM, R>::bytes(LB, UCfg<DIM, R>::TGM), h->stream>>>(
         U, h->Pr, h->St, h->g, ch, KZ, h->d_err, h->d_Bd, h->d_Bf, h->d_gat4, nullptr, xsp, h->Lb, tm);
     ring();
     dbg_sync(h, "k_states_u");
@@ -2014,7 +2014,7 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
   CK(cudaMemcpy(h->d_Bf, bf.data(), bf.size() * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_gat4, g4.data(), g4.size() * sizeof(int), cudaMemcpyHostToDevice));
   CK(cudaFuncSetAttribute(k_states_u<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)M::bytes(D == 3 && R == 2)));
+                          (int)M::bytes(D == 3 && R == 2, M::TGM)));
   if constexpr (D == 3 && R == 2)
     CK(cudaFuncSetAttribute(k_states_u<D, R, false, false, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M::bytes(true)));

@@ -66,7 +66,11 @@ struct UCfg {
   static constexpr int NDM = D == 3 ? G::NA / 8 : ND;
   static constexpr int NT = D == 3 ? G::NA - 8 * NDM : 0;
   static constexpr int NPT = (G::NP + 7) / 8;
-  static constexpr int RX = 32 + 2 * R;                 // region x extent
+  // region x extent (row stride): 32 + 2R columns are needed; 3-D R=3 keeps
+  // rows 42 words apart (bank model of its chunk tables, tools/bank_model.py:
+  // 2.4 wavefronts per A-operand load against 3.1 at 38)
+  static constexpr int RXN = 32 + 2 * R;
+  static constexpr int RX = (D == 3 && R == 3) ? 42 : RXN;
   static constexpr int RY = D == 3 ? 2 * R + 1 : 1;     // region mid extent
   static constexpr int RROW = RY * RX;                  // one variable of a plane
   static constexpr int PL = nv * RROW;                  // one region plane
@@ -90,8 +94,13 @@ struct UCfg {
   static constexpr int NG = (NPT + PG - 1) / PG;         // groups (>1: limiter separate)
   // LB: the instance whose limiter bounds come from k_bounds (3-D R=2 main
   // engine): no per-cell-quantity ring in shared memory
-  static constexpr size_t bytes(bool lb = false) {
-    return sizeof(double) * (RING * (lb ? (PL + 15) / 16 * 16 : PL) + (lb ? 0 : PRING * PPL) + 4 * SCW + SB) +
+  // TG: the instances that take the transform's per-cell quantities from Pr in
+  // global memory (no per-cell-quantity ring): LB, and the main 3-D instance
+  // of the configurations limited by k_limit_states (NG > 1: 3-D R=3, whose
+  // ring + per-cell-quantity ring allowed ONE 4-warp CTA per SM; without it two)
+  static constexpr bool TGM = D == 3 && NG > 1;
+  static constexpr size_t bytes(bool lb = false, bool tg = false) {
+    return sizeof(double) * (RING * (lb ? (PL + 15) / 16 * 16 : PL) + (lb || tg ? 0 : PRING * PPL) + 4 * SCW + SB) +
            (lb ? sizeof(unsigned long long) * (RING + 3) : 0) +
            sizeof(int) * (4 * G::NCHUNK * 2 + G::NCHUNK + 4 * NCH2) + KFVM_U_EXTRA_SMEM;
   }
@@ -129,6 +138,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   // the transform's per-cell quantities from Pr in global memory (no ring)
   constexpr bool LB = D == 3 && R == 2 && !P1 && !KXM && C::NG == 1;
   constexpr bool col = COL && LB;  // ring-column tile instance
+  constexpr bool TG = LB || (C::TGM && !P1 && !KXM);  // transform quantities from global Pr
   constexpr int nv = C::nv, NP = G::NP, NS = G::NS, ND = C::ND, NPT = C::NPT;
   // LB with a tensor map (tmap): the U planes arrive by TMA — one elected
   // thread, one 4-D box [var][row][x] per plane, an mbarrier per ring slot.
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
   extern __shared__ __align__(128) double smem[];
   double* sRing = smem;                          // [RING][nv][RY][RX]
   double* sPr = sRing + C::RING * SLk;         // [PRING][NF][NY][NX]
-  double* sC = sPr + (LB ? 0 : C::PRING * C::PPL);  // [warp][q][v][8]
+  double* sC = sPr + (TG ? 0 : C::PRING * C::PPL);  // [warp][q][v][8]
   double* sBd = sC + 4 * C::SCW;                 // B fragments [chunk][n][lane]
   double* sBf = sBd + G::NCHUNK * ND * 32;
   int* sTab = reinterpret_cast<int*>(sBd + C::SB);  // [chunk][4] {inplane, oz}
@@ -232,7 +242,8 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     for (int i = threadIdx.x; i < PLk; i += 128) {
       const int rx = i % RXk, rr = i / RXk;
       const int ry = rr % C::RY, v = rr / C::RY;
-      const int xx = xoff(g, x0 - R + rx);
+      // (padding columns of a wider row stride repeat the last needed one)
+      const int xx = xoff(g, x0 - R + (RXk > C::RXN ? min(rx, C::RXN - 1) : rx));
       const long long off = v * g.vstride + pbase + xx +
                             (D == 3 ? moff(g, j - R + ry) : 0);
       __pipeline_memcpy_async(dst + i, U + off, sizeof(double));
@@ -276,7 +287,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
       for (int oz = -R; oz <= R; ++oz) wait_plane(p + oz);
     } else {
       for (int oz = -R; oz <= R; ++oz) load_plane(p + oz);
-      if (!P1 && !LB)  // pass 1 needs neither the transform nor the limiter statistics
+      if (!P1 && !TG)  // pass 1 needs neither the transform nor the limiter statistics
         for (int oz = -1; oz <= 1; ++oz) load_prims(p + oz);
       __pipeline_commit();
       __pipeline_wait_prior(0);
@@ -295,7 +306,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     __pipeline_memcpy_async(sCw + f * 8 + (lane & 7),
                             Pr + (2 + f) * g.vstride + uidx<D>(g, ac - 1, jc, q), sizeof(double));
   };
-  if constexpr (LB) {
+  if constexpr (TG) {
     load_t(ch.c0 - 1 + cstart);
     __pipeline_commit();
     __pipeline_wait_prior(0);
@@ -313,7 +324,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     } else {
       if (c + 1 < cend) {
         load_plane(p + R + 1);
-        if (!P1 && !LB) load_prims(p + 2);
+        if (!P1 && !TG) load_prims(p + 2);
       }
       __pipeline_commit();
     }
@@ -355,11 +366,11 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     if (!LATE_RM) load_rm();
     // LB: the cell's per-cell quantities straight from Pr (the quad's lanes
     // load the same words)
-    T.inv_r = LB ? sCw[r8] : pr0[2 * C::PROW + icn];
+    T.inv_r = TG ? sCw[r8] : pr0[2 * C::PROW + icn];
     T.ut[2] = 0.0;
 #pragma unroll
-    for (int d = 0; d < D; ++d) T.ut[d] = LB ? sCw[(1 + d) * 8 + r8] : pr0[(3 + d) * C::PROW + icn];
-    if (LB) __syncwarp();  // every lane has its transform before pass 1 reuses sCw
+    for (int d = 0; d < D; ++d) T.ut[d] = TG ? sCw[(1 + d) * 8 + r8] : pr0[(3 + d) * C::PROW + icn];
+    if (TG) __syncwarp();  // every lane has its transform before pass 1 reuses sCw
     {
       double ke = T.ut[0] * T.ut[0];
       ke = fma(T.ut[1], T.ut[1], ke);
@@ -708,7 +719,7 @@ __global__ void __launch_bounds__(128, (P1 || KXM) ? (D == 3 && R == 2 ? 3 : UCf
     }
     }
     PHASE_MARK(3);
-    if constexpr (LB) {  // the next plane's transform quantities, hidden by the epilogue
+    if constexpr (TG) {  // the next plane's transform quantities, hidden by the epilogue
       __syncwarp();
 #ifndef KFVM_U_CTASYNC
       if (use_tma && lane == 0) mbar_arrive(&sDone[it & 1]);  // done with the oldest plane
