@@ -460,7 +460,8 @@ def main():
                     "serial_value": e2e_serial,
                     "serial_api": "Solver.set_state/ssp_rk3_step/get_state, one field, no overlap"},
             "roofline": {"bound": "fp64", "kernel": "k_states_* (reconstruction+WENO-AO+limiter)",
-                         "engine": "DMMA (FP64 tensor, plane-marching)" if g.dim == 3
+                         "engine": ("DMMA (FP64 tensor, plane-marching; 3-D R=2: the 16-warp W-cache "
+                                    "engine k_states_w where its TMA boxes apply)") if g.dim == 3
                          else "DFMA (unrolled, row-marching smem rings)",
                          # KXRCF mode: WENO runs only in flagged cells, so the
                          # WENO-everywhere flop count is not the work done
