@@ -1033,19 +1033,23 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
                                                                   h->d_err);
       h->launches++;
     }
-    // ring planes by TMA: the ring-split segments start on an even x
+    // ring planes by TMA: k_states_u needs segments that start on an even x
+    // (ring split); k_states_w's wider rows take either parity
+    const int ui = U == h->U0 ? 0 : (U == h->Ua ? 1 : (U == h->Ub ? 2 : -1));
     const CUtensorMap* tm = nullptr;
-    if (LB && xsp && h->tma && h->d_tmap)
-      tm = U == h->U0 ? h->d_tmap : (U == h->Ua ? h->d_tmap + 1 : (U == h->Ub ? h->d_tmap + 2 : nullptr));
+    if (LB && xsp && h->tma && h->d_tmap && ui >= 0) tm = h->d_tmap + ui;
     bool wide = false;
     if constexpr (LB) {
-      if (tm && h->wide && h->d_tmapw && h->d_gatw) {  // the 16-warp W-cache engine
+      if (h->tma && h->wide && h->d_tmapw && h->d_gatw && ui >= 0) {  // the 16-warp W-cache engine
         wide = true;
         const long long nbw = (long long)((ch.ex - 2 * xsp + 31) / 32) *
                               ((ch.em + kWideRows - 1) / kWideRows) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
-        k_states_w<kWideRows><<<(unsigned)nbw, 128 * kWideRows, WCfg<kWideRows>::bytes(), h->stream>>>(
-            h->Pr, h->St, h->g, ch, KZ, h->d_Bd, h->d_Bf, h->d_gatw, xsp, h->Lb,
-            h->d_tmapw + (tm - h->d_tmap));
+        if (xsp)
+          k_states_w<kWideRows, 0><<<(unsigned)nbw, 128 * kWideRows, WCfg<kWideRows>::bytes(), h->stream>>>(
+              h->Pr, h->St, h->g, ch, KZ, h->d_Bd, h->d_Bf, h->d_gatw, xsp, h->Lb, h->d_tmapw + ui);
+        else  // segments start at x = -1: the box one column earlier
+          k_states_w<kWideRows, 1><<<(unsigned)nbw, 128 * kWideRows, WCfg<kWideRows>::bytes(), h->stream>>>(
+              h->Pr, h->St, h->g, ch, KZ, h->d_Bd, h->d_Bf, h->d_gatw, xsp, h->Lb, h->d_tmapw + ui);
       }
     }
     if (!wide)
@@ -2004,7 +2008,9 @@ int upload_gen(kfvm_handle* h, const kfvm_table* t) {
     }
     CK(cudaMalloc(&h->d_gatw, gw.size() * sizeof(int)));
     CK(cudaMemcpy(h->d_gatw, gw.data(), gw.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaFuncSetAttribute(k_states_w<kWideRows>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_states_w<kWideRows, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)WC::bytes()));
+    CK(cudaFuncSetAttribute(k_states_w<kWideRows, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)WC::bytes()));
   }
   CK(cudaMalloc(&h->d_Bd, bd.size() * sizeof(double)));

@@ -61,7 +61,7 @@ struct WCfg {
 // table word of a chunk slot (host: upload_gen): region offset (oy+R)*RX+ox+R
 // | (oz+R) << 9 | stencil << 12 | W-cache position of the S0 cell << 16 | last
 // chunk of its stencil << 22
-template <int MR>
+template <int MR, int SH = 0>
 __global__ void __launch_bounds__(128 * MR, 1)
     k_states_w(const double* __restrict__ Pr, double* __restrict__ St, Geo g, Chunk ch, int KZ,
                const double* __restrict__ Bd, const double* __restrict__ Bf,
@@ -102,15 +102,19 @@ __global__ void __launch_bounds__(128 * MR, 1)
   const int j = bc - 1;
   const int cstart = ch.e0 + zblk * KZ, cend = min(ch.e1, cstart + KZ);
   const int x0 = xsp + seg * 32 - 1;
-  const int xr = cidx + R;
-  const int cb = wr * RX + cidx;             // the cell's offset in a region plane
+  // FP64 TMA boxes start on an even element: segments that start on an odd x
+  // (xsp = 0: they include the ring columns) load one more column on the left
+  // (the 42-word rows have the room) and shift the cell by one
+  constexpr int sh = SH;  // = (x0 - R) & 1 = !xsp (host; a run-time shift cost 2 % in registers)
+  const int xr = cidx + R + sh;
+  const int cb = wr * RX + cidx + sh;        // the cell's offset in a region plane
   const int icr = (R + wr) * RX + xr;        // the cell itself
 
   const int base = ch.c0 - 1 + cstart - R;
   auto tma_plane = [&](int q) {
     const int sl = (q + 4 * W::RING) % W::RING;
     mbar_expect_tx(&sBar[sl], (unsigned)(W::PL * sizeof(double)));
-    tma_load_4d(sRing + sl * SL, tmap, &sBar[sl], g.xo + x0 - R, rb * MR - 1 - R + g.Gm, q + g.H, 0);
+    tma_load_4d(sRing + sl * SL, tmap, &sBar[sl], g.xo + x0 - R - sh, rb * MR - 1 - R + g.Gm, q + g.H, 0);
   };
   auto wait_plane = [&](int q) {
     mbar_wait(&sBar[(q + 4 * W::RING) % W::RING], (unsigned)(((q - base) / W::RING) & 1));

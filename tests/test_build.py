@@ -52,7 +52,7 @@ def test_3d_wide_engine_fits_one_cta_per_sm():
     """k_states_w<4>: 512 threads at 128 registers (the whole register file of
     an SM) with a small documented spill (kfvm_recon_w.cuh)."""
     ks = kernels()
-    for k, (regs, st, ld) in pick(ks, re.escape("k_states_w<4>")).items():
+    for k, (regs, st, ld) in pick(ks, re.escape("k_states_w<4, ")).items():
         assert regs <= 128 and st <= 64 and ld <= 64, (k, regs, st, ld)
 
 

@@ -3,8 +3,8 @@ oracle and against k_states_u (option wide=0), bit for bit: row counts that
 leave a partial 4-row block (rows past the box are zero-filled by the TMA
 unit and never stored), periodic and outflow/wall sides, several z blocks
 (kz), the chunked stage schedule, and runs of several steps.  The engine
-applies where the ring-split segments start on an even x: nx = 32 k (or
-32 k - 1) or periodic x."""
+applies to every 3-D R=2 grid: ring-split segments (nx = 32 k or 32 k - 1,
+periodic x) start on an even x, the others one column earlier."""
 from dataclasses import replace
 
 import numpy as np
@@ -23,6 +23,8 @@ GRIDS = [
     (64, 13, 7, "outflow"),
     (32, 12, 8, "reflecting"),
     (40, 9, 8, "periodic"),   # periodic x: ring copy, interior segments (last one partial)
+    (40, 10, 8, "outflow"),   # no ring split: segments start at x = -1 (odd: shifted TMA box)
+    (100, 9, 7, "outflow"),
 ]
 
 
