@@ -711,6 +711,7 @@ struct kfvm_handle {
   CUtensorMap* d_tmapw = nullptr; // ... with the 16-warp engine's box (k_states_w: 2R+4 rows)
   int* d_gatw = nullptr;          // k_states_w's slot tables
   int wide = 1;                   // 3-D R=2: the 16-warp W-cache engine where its TMA boxes apply
+  int bounds_z = 1;               // 3-D R=2: k_bounds_z (plane-marching) instead of k_bounds
   int tma = 1;                    // option "tma": ring planes by TMA when the segments allow
   int ring_tiles = 1;             // option "ring_tiles": ring columns on the tensor engine
   size_t st_elems = 0, f_elems = 0, aos_elems = 0;
@@ -1028,9 +1029,15 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
         (long long)((ch.ex - 2 * xsp + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
     constexpr bool LB = DIM == 3 && R == 2;
     if (LB) {
-      const long long nw = (long long)((ch.ex + 29) / 30) * ch.em * (ch.e1 - ch.e0);
-      k_bounds<3><<<(unsigned)((nw + 3) / 4), 128, 0, h->stream>>>(U, h->Pr, h->Lb, h->g, ch,
-                                                                  h->d_err);
+      if (h->bounds_z) {  // warps march the planes (a third of the L2 reads)
+        const long long nw = (long long)((ch.ex + 29) / 30) * ch.em *
+                             ((ch.e1 - ch.e0 + kBoundsKB - 1) / kBoundsKB);
+        k_bounds_z<<<(unsigned)((nw + 3) / 4), 128, 0, h->stream>>>(U, h->Pr, h->Lb, h->g, ch, h->d_err);
+      } else {
+        const long long nw = (long long)((ch.ex + 29) / 30) * ch.em * (ch.e1 - ch.e0);
+        k_bounds<3><<<(unsigned)((nw + 3) / 4), 128, 0, h->stream>>>(U, h->Pr, h->Lb, h->g, ch,
+                                                                    h->d_err);
+      }
       h->launches++;
     }
     // ring planes by TMA: k_states_u needs segments that start on an even x
@@ -2857,6 +2864,11 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
   if (n == "tma") {
     drop_graphs(h);
     h->tma = value ? 1 : 0;
+    return KFVM_OK;
+  }
+  if (n == "bounds_z") {
+    drop_graphs(h);
+    h->bounds_z = value ? 1 : 0;
     return KFVM_OK;
   }
   if (n == "wide") {  // 3-D R=2: 1 = the 16-warp W-cache engine (k_states_w), 0 = k_states_u

@@ -1034,4 +1034,109 @@ __global__ void __launch_bounds__(128) k_bounds(const double* __restrict__ U,
   Lb[2 * ch.next + tid] = pmin;
 }
 
+// k_bounds_z: the same bounds with each warp marching KB planes of its row
+// segment along the slab axis: the (mid) row statistics of a plane are formed
+// once and kept in registers for the three planes that use them (k_bounds
+// re-reads every plane three times through L2: 9 instead of 27 neighbour
+// loads per cell and field).  min / max are exact, so the grouping is free.
+constexpr int kBoundsKB = 16;
+__device__ __forceinline__ void row_stats(const double* __restrict__ U,
+                                          const double* __restrict__ Pr, const Geo& g, int x,
+                                          int j, int p, double* st, double& rc, double& pc) {
+  st[0] = -INFINITY;
+  st[1] = INFINITY;
+  st[2] = INFINITY;
+  st[3] = INFINITY;
+#pragma unroll
+  for (int bb = -1; bb <= 1; ++bb) {
+    const long long o = uidx<3>(g, x, j + bb, p);
+    const double r = __ldg(U + o), pp = __ldg(Pr + o);
+    st[0] = fmax(st[0], r);
+    st[1] = fmin(st[1], r);
+    st[2] = fmin(st[2], pp);
+    st[3] = fmin(st[3], __ldg(Pr + g.vstride + o));
+    if (bb == 0) {
+      rc = r;
+      pc = pp;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) k_bounds_z(const double* __restrict__ U,
+                                                  const double* __restrict__ Pr,
+                                                  double* __restrict__ Lb, Geo g, Chunk ch,
+                                                  int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int nseg = (ch.ex + 29) / 30;
+  const int seg = (int)(wid % nseg);
+  const long long r1 = wid / nseg;
+  const int b = (int)(r1 % ch.em);
+  const int c0 = ch.e0 + (int)(r1 / ch.em) * kBoundsKB;
+  if (c0 >= ch.e1) return;  // whole warp
+  const int c1 = min(ch.e1, c0 + kBoundsKB);
+  const int a = min(seg * 30 - 1 + lane, ch.ex);  // column of this lane (a = -1 .. ex)
+  const int x = a - 1, j = b - 1;
+  const bool owner = !(lane == 0 || lane == 31 || a < 0 || a >= ch.ex);
+  // rolling rows of planes p - 1, p, p + 1: statistics, centre rho / p, w
+  double s0[4], s1[4], s2[4], r0, r1c, r2, q0, q1, q2, w0, w1, w2;
+  {
+    const int p = ch.c0 - 1 + c0;
+    row_stats(U, Pr, g, x, j, p - 1, s0, r0, q0);
+    row_stats(U, Pr, g, x, j, p, s1, r1c, q1);
+    w0 = __ldg(Pr + 5 * g.vstride + uidx<3>(g, x, j, p - 1));
+    w1 = __ldg(Pr + 5 * g.vstride + uidx<3>(g, x, j, p));
+  }
+  for (int c = c0; c < c1; ++c) {
+    const int p = ch.c0 - 1 + c;
+    row_stats(U, Pr, g, x, j, p + 1, s2, r2, q2);
+    w2 = __ldg(Pr + 5 * g.vstride + uidx<3>(g, x, j, p + 1));
+    const double u0 = __ldg(Pr + 3 * g.vstride + uidx<3>(g, x, j, p));
+    const double vp = __ldg(Pr + 4 * g.vstride + uidx<3>(g, x, j + 1, p));
+    const double vm = __ldg(Pr + 4 * g.vstride + uidx<3>(g, x, j - 1, p));
+    double own[4], lft[4], rgt[4];
+    own[0] = fmax(fmax(s0[0], s1[0]), s2[0]);
+#pragma unroll
+    for (int k = 1; k < 4; ++k) own[k] = fmin(fmin(s0[k], s1[k]), s2[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      lft[k] = __shfl_up_sync(0xffffffffu, own[k], 1);
+      rgt[k] = __shfl_down_sync(0xffffffffu, own[k], 1);
+    }
+    const double ul = __shfl_up_sync(0xffffffffu, u0, 1), ur = __shfl_down_sync(0xffffffffu, u0, 1);
+    if (owner) {
+      const double rt = r1c, pt = q1;
+      const double rbmax = fmax(fmax(own[0], lft[0]), rgt[0]);
+      const double rbmin = fmin(fmin(own[1], lft[1]), rgt[1]);
+      const double pbmin = fmin(fmin(own[2], lft[2]), rgt[2]);
+      const double cmin = fmin(fmin(own[3], lft[3]), rgt[3]);
+      double delta = 0.5 * (ur - ul);
+      delta = fma(0.5, vp - vm, delta);
+      delta = fma(0.5, w2 - w0, delta);
+      const double kc = c_k.kf * cmin;
+      double eta = -(delta + kc) / kc;
+      eta = fmin(1.0, fmax(0.0, eta));
+      const double fup = fma(c_k.kappa, 1.0 - eta, 1.0);
+      const double flo = fma(-c_k.kappa, 1.0 - eta, 1.0);
+      const double rmax = rbmax * fup, rmin = rbmin * flo, pmin = pbmin * flo;
+      if (!(rt > 0.0) || !(pt > 0.0) || !(rmin > 0.0) || !(pmin > 0.0)) atomicOr(err, 2);
+      const long long tid = ((long long)c * ch.em + b) * ch.ex + a;
+      Lb[tid] = rmax;
+      Lb[ch.next + tid] = rmin;
+      Lb[2 * ch.next + tid] = pmin;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      s0[k] = s1[k];
+      s1[k] = s2[k];
+    }
+    r0 = r1c;
+    r1c = r2;
+    q0 = q1;
+    q1 = q2;
+    w0 = w1;
+    w1 = w2;
+  }
+}
+
 #endif
