@@ -711,6 +711,8 @@ struct kfvm_handle {
   CUtensorMap* d_tmapw = nullptr; // ... with the 16-warp engine's box (k_states_w: 2R+4 rows)
   int* d_gatw = nullptr;          // k_states_w's slot tables
   int wide = 1;                   // 3-D R=2: the 16-warp W-cache engine where its TMA boxes apply
+  int kz_auto = 1;                // 3-D tensor engines: shorter z blocks on small grids (no kz option set)
+  int num_sm = 148;
   int bounds_z = 1;               // 3-D R=2: k_bounds_z (plane-marching) instead of k_bounds
   int tma = 1;                    // option "tma": ring planes by TMA when the segments allow
   int ring_tiles = 1;             // option "ring_tiles": ring columns on the tensor engine
@@ -1024,10 +1026,24 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
     }
   }
   if (h->engine == 2) {
-    const int KZ = h->kz;
+    constexpr bool LB = DIM == 3 && R == 2;
+    const int ui = U == h->U0 ? 0 : (U == h->Ua ? 1 : (U == h->Ub ? 2 : -1));
+    bool wide = false;
+    if constexpr (LB) wide = h->tma && h->wide && h->d_tmapw && h->d_gatw && ui >= 0;
+    // planes one CTA marches: kz (32), fewer on small grids so that the launch
+    // still has ~60 waves of CTAs (measured: 64^3 4.97 -> 3.1 ms/step, 128^3
+    // 16.3 -> 15.4, 256^3 103.3 -> 102.2, R=3 128^3 79.2 -> 75.6; >= 8: the
+    // ring fill per CTA); an explicit kz option is taken as given
+    int KZ = h->kz;
+    if (DIM == 3 && h->kz_auto) {
+      const long long per = (long long)((ch.ex - 2 * xsp + 31) / 32) *
+                            (wide ? (ch.em + kWideRows - 1) / kWideRows : ch.em);
+      const long long slots = (long long)h->num_sm * (wide ? 1 : UCfg<DIM, R>::MINB);
+      const long long k = (ch.e1 - ch.e0) * per / (60 * slots);
+      KZ = (int)std::max<long long>(std::min<long long>(8, h->kz), std::min<long long>(k, h->kz));
+    }
     const long long nblk2 =
         (long long)((ch.ex - 2 * xsp + 31) / 32) * ch.em * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
-    constexpr bool LB = DIM == 3 && R == 2;
     if (LB) {
       if (h->bounds_z) {  // warps march the planes (a third of the L2 reads)
         const long long nw = (long long)((ch.ex + 29) / 30) * ch.em *
@@ -1042,13 +1058,10 @@ void launch_states(kfvm_handle* h, const double* U, const Chunk& ch) {
     }
     // ring planes by TMA: k_states_u needs segments that start on an even x
     // (ring split); k_states_w's wider rows take either parity
-    const int ui = U == h->U0 ? 0 : (U == h->Ua ? 1 : (U == h->Ub ? 2 : -1));
     const CUtensorMap* tm = nullptr;
     if (LB && xsp && h->tma && h->d_tmap && ui >= 0) tm = h->d_tmap + ui;
-    bool wide = false;
     if constexpr (LB) {
-      if (h->tma && h->wide && h->d_tmapw && h->d_gatw && ui >= 0) {  // the 16-warp W-cache engine
-        wide = true;
+      if (wide) {  // the 16-warp W-cache engine
         const long long nbw = (long long)((ch.ex - 2 * xsp + 31) / 32) *
                               ((ch.em + kWideRows - 1) / kWideRows) * ((ch.e1 - ch.e0 + KZ - 1) / KZ);
         if (xsp)
@@ -2141,6 +2154,9 @@ extern "C" int kfvm_gpu_create(const kfvm_config* cfg, const kfvm_table* t, cons
     delete h;
     return KFVM_ERR_DEVICE;
   }
+  if (cudaDeviceGetAttribute(&h->num_sm, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess ||
+      h->num_sm < 1)
+    h->num_sm = 148;
   const int sa = cfg->dim - 1;
   h->nsa = sa == 2 ? cfg->nz : cfg->ny;
   if (h->nranks < 1 || h->nranks > h->nsa) {
@@ -2889,6 +2905,7 @@ extern "C" int kfvm_gpu_set_option(kfvm_handle* h, const char* name, long long v
   if (n == "kz") {
     if (value < 1) return fail(h, KFVM_ERR_CONFIG, "kz must be >= 1");
     h->kz = (int)value;
+    h->kz_auto = 0;
     drop_graphs(h);
     return fused3(h) ? configure_scratch(h, 0) : KFVM_OK;
   }
