@@ -2,10 +2,11 @@
 // (k_states_w): reconstruct_states with the pinned contract of
 // k_states_u (kfvm_recon_u.cuh), restructured around what
 // bounds it on B200 — the scalar FP64 instructions that share the datapath
-// with the DMMAs (profiles/r02/README.md).
+// with the DMMAs and the shared-memory wavefronts of the A-operand loads
+// (profiles/r02/README.md).
 //
 //  * CTA = 16 warps = MR = 4 adjacent rows x 32 cells, marching along z.  The
-//    four rows share one ring of region planes [var][2R+MR rows][36] (8 rows
+//    four rows share one ring of region planes [var][2R+MR rows][42] (8 rows
 //    for 4 instead of 5 for 1), each plane one TMA box.
 //  * W cache.  The A operand of a chunk slot is W = Phi_i U_k of the lane's
 //    cell i and stencil cell k.  A cell's stencil S0 has 33 cells but its 8
@@ -15,9 +16,13 @@
 //    operations of a slot) are stored in shared memory while pass 1 walks
 //    the chunks of stencil 0 (= S0, every stencil cell once) and every later
 //    slot of either pass reads them back: the same values, so the same bits.
-//    (The smaller ring is what makes room: 16 warps x 3 variables x 33 cells
-//    x 8 cells/warp x 8 B = 99 KB.)
-//  * No CTA barrier per plane (mbarrier hand-off as in k_states_u's TMA path).
+//    (The shared ring is what makes room: 16 warps x 3 variables x 33 cells
+//    x 8 cells/warp x 8 B = 99 KB of cache next to 79 KB of ring.)
+//  * Bank layout (tools/bank_model.py): rows 42 words apart, a warp's 8 cells
+//    contiguous, the cache split by half-warp with the S0 cells 4-coloured by
+//    the host so that the slots of a chunk fall in different bank windows.
+//  * No CTA barrier per plane (mbarrier hand-off as in k_states_u's TMA path);
+//    the rows run skewed in phase and the last row issues the TMAs.
 // Included inside namespace kfvm_b200 by kfvm_gpu.cu (after kfvm_recon_u.cuh).
 #ifndef KFVM_RECON_W_CUH_
 #define KFVM_RECON_W_CUH_
