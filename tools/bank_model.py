@@ -48,14 +48,19 @@ def ring(rx, cell):
     return lambda k4, e, r8: (off[e][1] + R) * rx + off[e][0] + R + cell(r8)
 
 
-print("ring loads (wavefronts per LDS.64: pass 1, pass 2)")
-for name, cm in (("cells w + 4 r8", lambda r: 4 * r), ("cells 8 w + r8", lambda r: r)):
-    for rx in (36, 38, 40, 42, 44):
-        print(f"  {name}  row stride {rx}: {wavefronts(ch1, ring(rx, cm)):.2f} "
-              f"{wavefronts(ch2, ring(rx, cm)):.2f}")
-print("W cache rows of 8 cells, S words apart (address S e + r8)")
-for S in (8, 12, 20):
-    f = lambda k4, e, r8, S=S: S * e + r8  # noqa: E731
-    print(f"  S = {S}: {wavefronts(ch1[K0:], f):.2f} {wavefronts(ch2, f):.2f}")
-print("W cache split by half-warp, position mod 4 = a 4-colouring of S0: the host's search "
-      "(kfvm_gpu.cu upload_gen) reaches ~1.2 wavefronts per half = 2.4 per load")
+def main():
+    print("ring loads (wavefronts per LDS.64: pass 1, pass 2)")
+    for name, cm in (("cells w + 4 r8", lambda r: 4 * r), ("cells 8 w + r8", lambda r: r)):
+        for rx in (36, 38, 40, 42, 44):
+            print(f"  {name}  row stride {rx}: {wavefronts(ch1, ring(rx, cm)):.2f} "
+                  f"{wavefronts(ch2, ring(rx, cm)):.2f}")
+    print("W cache rows of 8 cells, S words apart (address S e + r8)")
+    for S in (8, 12, 20):
+        f = lambda k4, e, r8, S=S: S * e + r8  # noqa: E731
+        print(f"  S = {S}: {wavefronts(ch1[K0:], f):.2f} {wavefronts(ch2, f):.2f}")
+    print("W cache split by half-warp, position mod 4 = a 4-colouring of S0: the host's search "
+          "(kfvm_gpu.cu upload_gen) reaches ~1.2 wavefronts per half = 2.4 per load")
+
+
+if __name__ == "__main__":
+    main()
